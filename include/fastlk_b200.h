@@ -1,0 +1,105 @@
+/*
+ * B200 extension API -- batched and device-resident detection.
+ *
+ * Not part of the reference ABI (the reference API is single-frame and
+ * host-only, fastlk.h:134-138). These entry points let a caller keep frames
+ * and results in HBM, run many frames per launch, pick the GPU, and express
+ * cell sizes the reference's 32*w x 2^(l-1)*h geometry cannot (e.g. 16x16,
+ * SURVEY §7 hard part 4). Results are bit-identical to flk_detector_run on
+ * each frame.
+ *
+ * Streams are passed as `void*` (a cudaStream_t; NULL = the legacy default
+ * stream). Device pointers are plain `uint8_t*` into the detector's device.
+ */
+#ifndef FASTLK_B200_EXT_H_
+#define FASTLK_B200_EXT_H_
+
+#include "fastlk.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Cell size override in level-0 pixels; 0 restores the reference geometry.
+ * Stored in the config but not a config-file key, so configs stay loadable
+ * by the reference. */
+FLK_API flk_status flkb_config_set_cell_size_px(flk_config* config, int cell_width_px,
+                                                int cell_height_px);
+
+/* GPU selection (default: the current device at flk_detector_create). */
+FLK_API flk_status flkb_detector_set_device(flk_detector* detector, int device);
+FLK_API int flkb_device_count(void);
+
+/* Many host frames in one call: images must all have the detector's frame
+ * size. outs[i] receives frame i's features (caller frees each); stats may be
+ * NULL or an array of n. Frames are pipelined through pinned staging buffers
+ * so H2D, compute and D2H overlap. */
+FLK_API flk_status flkb_detector_run_batch(flk_detector* detector,
+                                           const flk_image* const* images, int n,
+                                           flk_features** outs, flk_frame_stats* stats);
+
+/* ---------------------------------------------------------- device batches */
+
+/* A device-resident workspace for up to `capacity` frames of width x height
+ * (pyramid levels >= 1, per-frame cell keys and feature lists). */
+typedef struct flkb_batch flkb_batch;
+
+FLK_API flk_status flkb_batch_create(flk_detector* detector, int width, int height,
+                                     int capacity, flkb_batch** out);
+FLK_API void flkb_batch_destroy(flkb_batch* batch);
+
+/* Detects on `count` device frames: frame f row y starts at
+ * frames + f*frame_stride + y*row_pitch. Asynchronous on `stream`; results
+ * stay on the device until flkb_batch_download. with_stats fills per-frame
+ * nms_candidates / nms_comparisons (slower; off for throughput). */
+FLK_API flk_status flkb_batch_run_device(flkb_batch* batch, const uint8_t* frames,
+                                         size_t frame_stride, int row_pitch, int count,
+                                         int with_stats, void* stream);
+
+/* Same, from host memory: H2D copies of the frames happen inside the call on
+ * `stream` (pinned host memory overlaps; pageable is staged). */
+FLK_API flk_status flkb_batch_run_host(flkb_batch* batch, const uint8_t* frames,
+                                       size_t frame_stride, int row_pitch, int count,
+                                       void* stream);
+
+/* Copies per-frame counts and the compact feature lists to the host.
+ * features is count * flkb_batch_frame_capacity() entries; frame f's list
+ * starts at features + f*flkb_batch_frame_capacity(). Either may be NULL. */
+FLK_API flk_status flkb_batch_download(const flkb_batch* batch, int first, int count,
+                                       int* counts, flk_feature* features, void* stream);
+
+FLK_API int flkb_batch_frame_capacity(const flkb_batch* batch); /* grid cells per frame */
+FLK_API const int* flkb_batch_device_counts(const flkb_batch* batch);
+FLK_API const flk_feature* flkb_batch_device_features(const flkb_batch* batch);
+/* Device stats: per frame {uint64 candidates, uint64 comparisons}. */
+FLK_API const uint64_t* flkb_batch_device_stats(const flkb_batch* batch);
+
+/* The pyramid product on the device (level >= 1; level 0 is the input). */
+FLK_API flk_status flkb_batch_device_pyramid(const flkb_batch* batch, int level,
+                                             const uint8_t** base, int* width, int* height,
+                                             int* row_pitch, size_t* frame_stride);
+
+/* Deterministic synthetic frames written on the device:
+ * kind 0 = S1 noise, 1 = S2 texture; frame f gets index first_frame + f. */
+FLK_API flk_status flkb_synth_frames_device(uint8_t* frames, int kind, uint64_t first_frame,
+                                            int count, int width, int height, int row_pitch,
+                                            size_t frame_stride, void* stream);
+
+/* Corner-response maps of every pyramid level for one frame (the values of
+ * the reference's detect_responses, fast.cpp:273-303), tightly packed
+ * level after level as floats: sum_k w_k*h_k entries. A diagnostic entry
+ * point for parity tests; subject to the detector's frame-size latch. */
+FLK_API flk_status flkb_detector_responses(flk_detector* detector, const flk_image* image,
+                                           float* out);
+
+/* Number of CUDA kernels this library has launched in the process (graph
+ * replays count every kernel node). */
+FLK_API uint64_t flkb_kernel_launch_count(void);
+/* Kernels one flkb_batch_run_device call launches (without stats). */
+FLK_API int flkb_batch_kernels_per_run(const flkb_batch* batch);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* FASTLK_B200_EXT_H_ */

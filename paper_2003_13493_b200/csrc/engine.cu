@@ -1,0 +1,344 @@
+// Host orchestration of the sm_100a detector kernels: geometry, device
+// buffers, launch plan, stage timing, conformance and synthetic frames.
+#include <atomic>
+#include <cstddef>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "conformance.cuh"
+#include "engine.hpp"
+#include "kernels_v1.cuh"
+
+namespace flkb {
+
+namespace {
+
+std::atomic<uint64_t> g_launches{0};
+
+size_t round_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+template <typename T>
+T* dalloc(size_t n, const char* what) {
+  void* p = nullptr;
+  check_cuda(cudaMalloc(&p, n * sizeof(T) + 16), what);
+  return static_cast<T*>(p);
+}
+
+using FastFn = void (*)(const uint8_t*, int, size_t, int, int, int, uint16_t*, int, size_t);
+
+template <int N>
+FastFn fast_for_kind(int kind) {
+  switch (kind) {
+    case kSadB: return k_fast_map<N, kSadB>;
+    case kSadA: return k_fast_map<N, kSadA>;
+    default: return k_fast_map<N, kMt>;
+  }
+}
+
+FastFn fast_kernel(int n, int kind) {
+  switch (n) {
+    case 9: return fast_for_kind<9>(kind);
+    case 10: return fast_for_kind<10>(kind);
+    case 11: return fast_for_kind<11>(kind);
+    case 12: return fast_for_kind<12>(kind);
+    case 13: return fast_for_kind<13>(kind);
+    case 14: return fast_for_kind<14>(kind);
+    case 15: return fast_for_kind<15>(kind);
+    default: return fast_for_kind<16>(kind);
+  }
+}
+
+}  // namespace
+
+void check_cuda(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) {
+    throw DeviceError(std::string("CUDA error in ") + what + ": " + cudaGetErrorString(e));
+  }
+}
+
+uint64_t launch_count() { return g_launches.load(); }
+void count_launches(int n) { g_launches += static_cast<uint64_t>(n); }
+
+DeviceGuard::DeviceGuard(int device) {
+  check_cuda(cudaGetDevice(&prev_), "cudaGetDevice");
+  if (prev_ != device) check_cuda(cudaSetDevice(device), "cudaSetDevice");
+}
+DeviceGuard::~DeviceGuard() {
+  int cur = -1;
+  if (cudaGetDevice(&cur) == cudaSuccess && cur != prev_ && prev_ >= 0) cudaSetDevice(prev_);
+}
+
+DetectParams DetectParams::from(const Config& c) {
+  DetectParams p;
+  p.epsilon = c.epsilon;
+  p.arc_length = c.arc_length;
+  p.score = static_cast<int>(c.score);
+  p.levels = c.num_levels;
+  p.radius = c.nms_radius;
+  p.cell_w = c.cell_width();
+  p.cell_h = c.cell_height();
+  return p;
+}
+
+Geometry Geometry::make(const DetectParams& p, int width, int height) {
+  if (p.levels < 1 || p.levels > kMaxLevels)
+    throw InvalidArgument("pyramid needs between 1 and 16 levels");
+  if (width < 1 || height < 1) throw InvalidArgument("image dimensions must be positive");
+  if ((std::min(width, height) >> (p.levels - 1)) < 8)
+    throw InvalidArgument("image " + std::to_string(width) + "x" + std::to_string(height) +
+                          " too small for " + std::to_string(p.levels) + " pyramid levels");
+  if (width >= (1 << kCoordBits) || height >= (1 << kCoordBits))
+    throw InvalidArgument("frames are limited to 262143 pixels per side");
+  Geometry g;
+  g.width = width;
+  g.height = height;
+  g.levels = p.levels;
+  int w = width, h = height;
+  size_t off = 0;
+  for (int k = 0; k < p.levels; ++k) {
+    g.lw[k] = w;
+    g.lh[k] = h;
+    g.lpitch[k] = static_cast<int>(round_up(static_cast<size_t>(w), 16));
+    if (k > 0) {
+      g.loff[k] = off;
+      off += static_cast<size_t>(g.lpitch[k]) * h;
+    }
+    w /= 2;
+    h /= 2;
+  }
+  g.pyr_frame_bytes = round_up(off, 256);
+  g.cols = (width + p.cell_w - 1) / p.cell_w;
+  g.rows = (height + p.cell_h - 1) / p.cell_h;
+  g.cells = g.cols * g.rows;
+  return g;
+}
+
+DeviceBatch::DeviceBatch(const DetectParams& p, int device, int width, int height, int capacity)
+    : p_(p), g_(Geometry::make(p, width, height)), device_(device), capacity_(capacity) {
+  if (capacity < 1) throw InvalidArgument("batch capacity must be positive");
+  DeviceGuard guard(device_);
+  size_t resp = 0;
+  for (int k = 0; k < g_.levels; ++k) resp += static_cast<size_t>(g_.lpitch[k]) * g_.lh[k];
+  resp_frame_elems_ = round_up(resp, 128);
+  const size_t cap = static_cast<size_t>(capacity_);
+  if (g_.pyr_frame_bytes) d_pyr_ = dalloc<uint8_t>(g_.pyr_frame_bytes * cap, "pyramid");
+  d_resp_ = dalloc<uint16_t>(resp_frame_elems_ * cap, "responses");
+  d_keys_ = dalloc<unsigned long long>(static_cast<size_t>(g_.cells) * cap, "cell keys");
+  d_feats_ = dalloc<flk_feature>(static_cast<size_t>(g_.cells) * cap, "features");
+  d_counts_ = dalloc<int>(cap, "counts");
+  d_stats_ = dalloc<uint64_t>(2 * cap, "stats");
+  check_cuda(cudaMemset(d_keys_, 0, sizeof(unsigned long long) * g_.cells * cap), "memset keys");
+  check_cuda(cudaMemset(d_counts_, 0, sizeof(int) * cap), "memset counts");
+  check_cuda(cudaMemset(d_stats_, 0, sizeof(uint64_t) * 2 * cap), "memset stats");
+}
+
+DeviceBatch::~DeviceBatch() {
+  int cur = -1;
+  cudaGetDevice(&cur);
+  cudaSetDevice(device_);
+  cudaFree(d_pyr_);
+  cudaFree(d_resp_);
+  cudaFree(d_keys_);
+  cudaFree(d_feats_);
+  cudaFree(d_counts_);
+  cudaFree(d_stats_);
+  cudaFree(d_naive_);
+  cudaFree(d_conf_);
+  if (cur >= 0) cudaSetDevice(cur);
+}
+
+int DeviceBatch::kernels_per_run() const { return 3 * g_.levels; }
+
+void DeviceBatch::run(const uint8_t* frames, size_t fstride, int pitch, int count, bool stats,
+                      cudaStream_t s, StageTimes* times, int first) {
+  if (count < 1 || first < 0 || first + count > capacity_)
+    throw InvalidArgument("batch count " + std::to_string(count) + " outside [1, " +
+                          std::to_string(capacity_) + "]");
+  if (pitch < g_.width) throw InvalidArgument("row pitch smaller than the frame width");
+  DeviceGuard guard(device_);
+  cudaEvent_t ev[4] = {};
+  if (times) {
+    for (auto& e : ev) check_cuda(cudaEventCreate(&e), "cudaEventCreate");
+    check_cuda(cudaEventRecord(ev[0], s), "cudaEventRecord");
+  }
+  // outputs of frame f land in slot first + f
+  uint8_t* pyr = d_pyr_ ? d_pyr_ + static_cast<size_t>(first) * g_.pyr_frame_bytes : nullptr;
+  uint16_t* respb = d_resp_ + static_cast<size_t>(first) * resp_frame_elems_;
+  unsigned long long* keys = d_keys_ + static_cast<size_t>(first) * g_.cells;
+  flk_feature* feats = d_feats_ + static_cast<size_t>(first) * g_.cells;
+  int* counts = d_counts_ + first;
+  unsigned long long* st = reinterpret_cast<unsigned long long*>(d_stats_ + 2 * static_cast<size_t>(first));
+  if (stats) check_cuda(cudaMemsetAsync(st, 0, sizeof(uint64_t) * 2 * count, s), "memset stats");
+
+  // level k's image: base pointer, pitch, frame stride
+  auto level_ptr = [&](int k) -> const uint8_t* { return k == 0 ? frames : pyr + g_.loff[k]; };
+  auto level_pitch = [&](int k) { return k == 0 ? pitch : g_.lpitch[k]; };
+  auto level_fs = [&](int k) { return k == 0 ? fstride : g_.pyr_frame_bytes; };
+
+  int launched = 0;
+  for (int k = 1; k < g_.levels; ++k) {
+    const int wd = g_.lw[k], hd = g_.lh[k];
+    const uint8_t* src = level_ptr(k - 1);
+    const int vec_ok = (reinterpret_cast<uintptr_t>(src) % 16 == 0) && level_pitch(k - 1) % 16 == 0 &&
+                       level_fs(k - 1) % 16 == 0;
+    dim3 block(32, 8), grid((wd + 255) / 256, (hd + 7) / 8, count);
+    k_pyramid_down<<<grid, block, 0, s>>>(src, level_pitch(k - 1), level_fs(k - 1),
+                                          pyr + g_.loff[k], g_.lpitch[k], g_.pyr_frame_bytes,
+                                          wd, hd, vec_ok);
+    ++launched;
+  }
+  if (times) check_cuda(cudaEventRecord(ev[1], s), "cudaEventRecord");
+
+  size_t roff = 0;
+  size_t roffs[kMaxLevels];
+  const FastFn fast = fast_kernel(p_.arc_length, p_.score);
+  for (int k = 0; k < g_.levels; ++k) {
+    roffs[k] = roff;
+    dim3 block(64, 4), grid((g_.lw[k] + 63) / 64, (g_.lh[k] + 3) / 4, count);
+    fast<<<grid, block, 0, s>>>(level_ptr(k), level_pitch(k), level_fs(k), g_.lw[k], g_.lh[k],
+                                p_.epsilon, respb + roff, g_.lpitch[k], resp_frame_elems_);
+    roff += static_cast<size_t>(g_.lpitch[k]) * g_.lh[k];
+    ++launched;
+  }
+  if (times) check_cuda(cudaEventRecord(ev[2], s), "cudaEventRecord");
+
+  for (int k = 0; k < g_.levels; ++k) {
+    dim3 block(64, 4), grid((g_.lw[k] + 63) / 64, (g_.lh[k] + 3) / 4, count);
+    if (stats)
+      k_nms_select<true><<<grid, block, 0, s>>>(respb + roffs[k], g_.lpitch[k], resp_frame_elems_,
+                                                g_.lw[k], g_.lh[k], k, p_.radius, p_.cell_w,
+                                                p_.cell_h, g_.cols, g_.cells, keys, st);
+    else
+      k_nms_select<false><<<grid, block, 0, s>>>(respb + roffs[k], g_.lpitch[k], resp_frame_elems_,
+                                                 g_.lw[k], g_.lh[k], k, p_.radius, p_.cell_w,
+                                                 p_.cell_h, g_.cols, g_.cells, keys, nullptr);
+    ++launched;
+  }
+  k_compact<<<count, 256, 0, s>>>(keys, g_.cols, g_.cells, feats, counts);
+  ++launched;
+  check_cuda(cudaGetLastError(), "kernel launch");
+  count_launches(launched);
+  if (times) {
+    check_cuda(cudaEventRecord(ev[3], s), "cudaEventRecord");
+    check_cuda(cudaEventSynchronize(ev[3]), "cudaEventSynchronize");
+    float a = 0, b = 0, c = 0;
+    cudaEventElapsedTime(&a, ev[0], ev[1]);
+    cudaEventElapsedTime(&b, ev[1], ev[2]);
+    cudaEventElapsedTime(&c, ev[2], ev[3]);
+    times->pyramid_us = a * 1e3;
+    times->crf_us = b * 1e3;
+    times->nms_us = c * 1e3;
+    for (auto& e : ev) cudaEventDestroy(e);
+  }
+}
+
+void DeviceBatch::download(int first, int count, int* counts, flk_feature* feats,
+                           cudaStream_t s) const {
+  if (first < 0 || count < 0 || first + count > capacity_)
+    throw InvalidArgument("download range outside the batch");
+  DeviceGuard guard(device_);
+  if (counts)
+    check_cuda(cudaMemcpyAsync(counts, d_counts_ + first, sizeof(int) * count,
+                               cudaMemcpyDeviceToHost, s), "download counts");
+  if (feats)
+    check_cuda(cudaMemcpyAsync(feats, d_feats_ + static_cast<size_t>(first) * g_.cells,
+                               sizeof(flk_feature) * g_.cells * count, cudaMemcpyDeviceToHost, s),
+               "download features");
+}
+
+void DeviceBatch::download_responses(int frame, float* out, cudaStream_t s) const {
+  DeviceGuard guard(device_);
+  std::vector<uint16_t> tmp(resp_frame_elems_);
+  check_cuda(cudaMemcpyAsync(tmp.data(), d_resp_ + static_cast<size_t>(frame) * resp_frame_elems_,
+                             sizeof(uint16_t) * resp_frame_elems_, cudaMemcpyDeviceToHost, s),
+             "download responses");
+  check_cuda(cudaStreamSynchronize(s), "responses sync");
+  size_t roff = 0;
+  for (int k = 0; k < g_.levels; ++k) {
+    for (int y = 0; y < g_.lh[k]; ++y)
+      for (int x = 0; x < g_.lw[k]; ++x)
+        *out++ = static_cast<float>(tmp[roff + static_cast<size_t>(y) * g_.lpitch[k] + x]);
+    roff += static_cast<size_t>(g_.lpitch[k]) * g_.lh[k];
+  }
+}
+
+flk_conformance DeviceBatch::conformance(const uint8_t* frames, size_t fstride, int pitch,
+                                         cudaStream_t s) {
+  (void)fstride;
+  DeviceGuard guard(device_);
+  size_t total = 0;
+  for (int k = 0; k < g_.levels; ++k) total += static_cast<size_t>(g_.lw[k]) * g_.lh[k];
+  // tally[3] | level widths[16] | level heights[16] | map pointers[16]
+  constexpr size_t kTallyBytes = 3 * sizeof(int) + 2 * kMaxLevels * sizeof(int) + 4;
+  if (!d_naive_) d_naive_ = dalloc<float>(total, "conformance maps");
+  if (!d_conf_) d_conf_ = dalloc<int>((kTallyBytes + kMaxLevels * sizeof(float*)) / sizeof(int) + 4,
+                                      "conformance tally");
+  struct Tables {
+    int tally[3];
+    int lw[kMaxLevels];
+    int lh[kMaxLevels];
+    int pad;
+    const float* maps[kMaxLevels];
+  } t{};
+  static_assert(offsetof(Tables, maps) % 8 == 0, "pointer alignment");
+  size_t off = 0;
+  int launched = 0;
+  for (int k = 0; k < g_.levels; ++k) {
+    t.lw[k] = g_.lw[k];
+    t.lh[k] = g_.lh[k];
+    t.maps[k] = d_naive_ + off;
+    off += static_cast<size_t>(g_.lw[k]) * g_.lh[k];
+  }
+  Tables* dt = reinterpret_cast<Tables*>(d_conf_);
+  check_cuda(cudaMemcpyAsync(dt, &t, sizeof(Tables), cudaMemcpyHostToDevice, s), "upload tables");
+  for (int k = 0; k < g_.levels; ++k) {
+    const uint8_t* img = k == 0 ? frames : d_pyr_ + g_.loff[k];
+    const int ip = k == 0 ? pitch : g_.lpitch[k];
+    dim3 block(32, 8), grid((g_.lw[k] + 31) / 32, (g_.lh[k] + 7) / 8);
+    k_naive_fast<<<grid, block, 0, s>>>(img, ip, g_.lw[k], g_.lh[k], p_.epsilon, p_.arc_length,
+                                        p_.score, const_cast<float*>(t.maps[k]));
+    k_naive_survivors<<<grid, block, 0, s>>>(t.maps[k], g_.lw[k], g_.lh[k], p_.radius,
+                                             dt->tally);
+    launched += 2;
+  }
+  k_conf_features<<<(g_.cells + 127) / 128, 128, 0, s>>>(d_feats_, d_counts_, dt->maps, dt->lw,
+                                                         dt->lh, p_.radius, dt->tally);
+  ++launched;
+  check_cuda(cudaGetLastError(), "conformance launch");
+  count_launches(launched);
+  int host[3] = {0, 0, 0};
+  check_cuda(cudaMemcpyAsync(host, dt->tally, sizeof(host), cudaMemcpyDeviceToHost, s), "tally");
+  check_cuda(cudaStreamSynchronize(s), "conformance sync");
+  flk_conformance c;
+  c.matched = host[1];
+  c.false_positives = host[2];
+  c.subset_only = host[0] - host[1];
+  return c;
+}
+
+namespace {
+__global__ void k_synth(uint8_t* out, int kind, uint64_t first, int w, int h, int pitch,
+                        size_t fs) {
+  const int x = blockIdx.x * blockDim.x + threadIdx.x;
+  const int y = blockIdx.y * blockDim.y + threadIdx.y;
+  const int f = blockIdx.z;
+  if (x >= w || y >= h) return;
+  out[f * fs + static_cast<size_t>(y) * pitch + x] = synth_pixel(kind, first + f, x, y, w);
+}
+}  // namespace
+
+void synth_frames(uint8_t* frames, int kind, uint64_t first, int count, int width, int height,
+                  int pitch, size_t fs, cudaStream_t s) {
+  if (kind < 0 || kind > 1) throw InvalidArgument("synthetic kind must be 0 (noise) or 1 (texture)");
+  dim3 block(64, 4);
+  for (int c0 = 0; c0 < count; c0 += 65535) {
+    const int n = std::min(65535, count - c0);
+    dim3 grid((width + 63) / 64, (height + 3) / 4, n);
+    k_synth<<<grid, block, 0, s>>>(frames + c0 * fs, kind, first + c0, width, height, pitch, fs);
+    count_launches(1);
+  }
+  check_cuda(cudaGetLastError(), "synth launch");
+}
+
+}  // namespace flkb

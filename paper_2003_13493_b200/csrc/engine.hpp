@@ -1,0 +1,120 @@
+// Device-side engine: geometry, HBM layout and the launch plan for one
+// detector configuration and frame size.
+//
+// HBM layout per batch of `capacity` frames (all frame slots contiguous):
+//   input        caller-owned: frame f row y at in + f*frame_stride + y*pitch
+//   pyramid      levels >= 1, frame slot = sum_k pitch_k*h_k bytes, pitch_k
+//                = roundup(w_k, 16) so every row starts 16-B aligned
+//   responses    v1 path only: u16 score maps, same geometry as the pyramid
+//   cell keys    u64 per grid cell, packed (score, -level, -y0, -x0); zero =
+//                empty. Reset by the compaction kernel after it reads them.
+//   features     flk_feature[cells] per frame, row-major cell order
+//   counts       int per frame
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <memory>
+#include <string>
+
+#include "../../include/fastlk.h"
+#include "common.hpp"
+
+namespace flkb {
+
+constexpr int kMaxLevels = 16;
+constexpr int kCoordBits = 18;  // x0, y0 < 2^18 inside a packed cell key
+
+struct DetectParams {
+  int epsilon = 10;
+  int arc_length = 10;
+  int score = 0;  // ScoreKind
+  int levels = 1;
+  int radius = 1;
+  int cell_w = 32;
+  int cell_h = 32;
+  static DetectParams from(const Config& c);
+};
+
+struct Geometry {
+  int width = 0, height = 0, levels = 0;
+  int lw[kMaxLevels] = {}, lh[kMaxLevels] = {}, lpitch[kMaxLevels] = {};
+  size_t loff[kMaxLevels] = {};  // byte offset of level k inside a frame's pyramid slot
+  size_t pyr_frame_bytes = 0;    // levels >= 1
+  int cols = 0, rows = 0, cells = 0;
+  // build_pyramid's size rule (image.cpp:37-45) -> InvalidArgument.
+  static Geometry make(const DetectParams& p, int width, int height);
+};
+
+struct StageTimes {
+  double pyramid_us = 0, crf_us = 0, nms_us = 0;
+};
+
+// Restores the caller's current device on scope exit.
+class DeviceGuard {
+ public:
+  explicit DeviceGuard(int device);
+  ~DeviceGuard();
+
+ private:
+  int prev_ = -1;
+};
+
+void check_cuda(cudaError_t e, const char* what);
+uint64_t launch_count();
+void count_launches(int n);
+
+class DeviceBatch {
+ public:
+  DeviceBatch(const DetectParams& p, int device, int width, int height, int capacity);
+  ~DeviceBatch();
+  DeviceBatch(const DeviceBatch&) = delete;
+  DeviceBatch& operator=(const DeviceBatch&) = delete;
+
+  // Enqueue detection of `count` device frames on `stream`. With `stats`
+  // the per-frame counters are produced (slower kernels). With `times` the
+  // call synchronizes and reports per-stage device time.
+  void run(const uint8_t* frames, size_t frame_stride, int pitch, int count, bool stats,
+           cudaStream_t stream, StageTimes* times = nullptr, int first = 0);
+  void download(int first, int count, int* counts, flk_feature* feats, cudaStream_t s) const;
+  // Score maps of frame `frame` of the last run, every level, tightly packed
+  // floats (the reference's ResponseMap values). Synchronous.
+  void download_responses(int frame, float* out, cudaStream_t s) const;
+  // Naive GPU conformance tally (oracle.cpp:240-268 semantics) for frame 0
+  // of the last run; frames pointer/pitch as passed to run().
+  flk_conformance conformance(const uint8_t* frames, size_t frame_stride, int pitch,
+                              cudaStream_t s);
+
+  const Geometry& geometry() const { return g_; }
+  const DetectParams& params() const { return p_; }
+  int capacity() const { return capacity_; }
+  int device() const { return device_; }
+  int kernels_per_run() const;
+  const int* device_counts() const { return d_counts_; }
+  const flk_feature* device_features() const { return d_feats_; }
+  const uint64_t* device_stats() const { return d_stats_; }
+  const uint8_t* device_pyramid() const { return d_pyr_; }
+  uint8_t* mutable_pyramid() { return d_pyr_; }
+
+ private:
+  DetectParams p_;
+  Geometry g_;
+  int device_ = 0;
+  int capacity_ = 0;
+  uint8_t* d_pyr_ = nullptr;
+  uint16_t* d_resp_ = nullptr;
+  size_t resp_frame_elems_ = 0;
+  unsigned long long* d_keys_ = nullptr;
+  flk_feature* d_feats_ = nullptr;
+  int* d_counts_ = nullptr;
+  uint64_t* d_stats_ = nullptr;  // [capacity][2] = candidates, comparisons
+  float* d_naive_ = nullptr;     // conformance scratch (lazily allocated)
+  int* d_conf_ = nullptr;
+};
+
+// Device synthetic generator, bit-identical to tests/synth.py.
+void synth_frames(uint8_t* frames, int kind, uint64_t first, int count, int width, int height,
+                  int pitch, size_t frame_stride, cudaStream_t s);
+
+}  // namespace flkb

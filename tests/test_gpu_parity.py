@@ -1,0 +1,211 @@
+"""Parity of the CUDA path with the CPU oracle, through the C ABI (GPU only).
+
+Bit-exact on every byte/integer output: feature lists (x, y, score, level,
+cell), per-level score maps, pyramid levels, the deterministic counters
+(nms_candidates, nms_comparisons) and the conformance tally.
+"""
+import hashlib
+
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from cases import GOLDEN
+
+pytestmark = pytest.mark.gpu
+
+fl = pytest.importorskip("paper_2003_13493_b200")
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _need_gpu():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+def make_config(cfg):
+    c = fl.Config(epsilon=cfg["epsilon"], N=cfg["N"], score_kind=cfg["score_kind"],
+                  l=cfg["l"], w=cfg["w"], h=cfg["h"], n=cfg["n"])
+    if cfg.get("cell_width_px") or cfg.get("cell_height_px"):
+        c.set_cell_size_px(cfg.get("cell_width_px", 0), cfg.get("cell_height_px", 0))
+    return c
+
+
+@pytest.mark.parametrize("case", GOLDEN, ids=[c[0] for c in GOLDEN])
+def test_golden_cases_through_c_abi(golden, case):
+    meta, arrays = golden
+    name, fam, f, w, h, cfg, full = case
+    m = meta[name]
+    img = synth.frame(fam, f, w, h)
+    det = fl.Detector(make_config(cfg))
+    feats, extra = det.run(img, stats=True)
+    assert len(feats) == m["count"]
+    assert hashlib.sha256(feats.tobytes()).hexdigest() == m["sha256"]
+    if full:
+        assert (feats == arrays[name]).all()
+    st = extra["stats"]
+    assert st["nms_candidates"] == m["candidates"]
+    assert st["nms_comparisons"] == m["comparisons"]
+    assert st["feature_count"] == m["count"]
+    # the graph-replayed, stats-free path gives the same list
+    again = det.run(img)
+    assert (again == feats).all()
+
+
+@pytest.mark.parametrize("seed", range(16))
+def test_random_configs_vs_oracle(orc, seed):
+    rng = np.random.default_rng(500 + seed)
+    l = int(rng.integers(1, 5))
+    w = int(rng.integers(8 << (l - 1), 400))
+    h = int(rng.integers(8 << (l - 1), 300))
+    fam = ["noise", "texture", "quant4", "blocks"][seed % 4]
+    img = synth.frame(fam, seed, w, h)
+    cfg = dict(epsilon=int(rng.choice([0, 1, 5, 10, 25, 80, 255])), N=int(rng.integers(9, 17)),
+               score_kind=["sad_b", "sad_a", "mt"][seed % 3], l=l, w=int(rng.integers(1, 3)),
+               h=int(rng.integers(1, 9)), n=int(rng.integers(1, 5)))
+    p = oracle.make_params(**cfg)
+    det = fl.Detector(make_config(cfg))
+    resp = det.responses(img, l)
+    for k, (a, b) in enumerate(zip(resp, orc.responses(img, p))):
+        assert (a == b).all(), f"level {k} score map differs"
+    det2 = fl.Detector(make_config(cfg))
+    feats, extra = det2.run(img, stats=True)
+    ref, st = orc.detect(img, p)
+    assert (feats == ref).all()
+    assert extra["stats"]["nms_candidates"] == st.candidates
+    assert extra["stats"]["nms_comparisons"] == st.comparisons
+
+
+@pytest.mark.parametrize("kind", ["sad_b", "sad_a", "mt"])
+@pytest.mark.parametrize("n", range(9, 17))
+def test_arc_test_exhaustive_on_device(orc, kind, n):
+    """Every 16-bit dark and bright mask, each in its own 7x7 box, scored on
+    the GPU: corner iff the rotation-scan oracle finds a run >= N
+    (acceptance.cpp:72-84), and the score equals the oracle's."""
+    boxes = 256
+    img = np.full((7 * boxes, 7 * boxes), 128, np.uint8)
+    ring = [(0, -3), (1, -3), (2, -2), (3, -1), (3, 0), (3, 1), (2, 2), (1, 3),
+            (0, 3), (-1, 3), (-2, 2), (-3, 1), (-3, 0), (-3, -1), (-2, -2), (-1, -3)]
+    masks = np.arange(65536)
+    by, bx = np.divmod(masks, boxes)
+    cy, cx = 7 * by + 3, 7 * bx + 3
+    for bright in (False, True):
+        im = img.copy()
+        for i, (dx, dy) in enumerate(ring):
+            on = ((masks >> i) & 1).astype(bool)
+            # dark ring value 60 +- a little so SAD/MT are not constant
+            val = (200 + (masks % 40)) if bright else (60 - (masks % 40))
+            im[cy[on] + dy, cx[on] + dx] = val[on].astype(np.uint8)
+        p = oracle.make_params(epsilon=10, N=n, score_kind=kind)
+        det = fl.Detector(fl.Config(epsilon=10, N=n, score_kind=kind))
+        got = det.responses(im, 1)[0][cy, cx]
+        expect = np.array([orc.arc_oracle(int(m), n) for m in masks])
+        assert ((got > 0) == expect).all()
+        want = orc.fast_level(im, p)[cy, cx]
+        assert (got == want).all()
+
+
+class _DevBuf:
+    """Raw device bytes viewed through __cuda_array_interface__ (torch reads it)."""
+
+    def __init__(self, ptr: int, nbytes: int):
+        self.__cuda_array_interface__ = {"shape": (nbytes,), "typestr": "|u1",
+                                         "data": (ptr, True), "version": 3}
+
+
+def read_device(ptr: int, nbytes: int) -> np.ndarray:
+    import torch
+    return torch.as_tensor(_DevBuf(ptr, nbytes), device="cuda").cpu().numpy()
+
+
+def test_pyramid_levels_match_oracle(orc):
+    import torch
+    W, H, L = 753, 481, 4
+    frames = np.stack([synth.texture(i, W, H) for i in range(3)])
+    det = fl.Detector(fl.Config(l=L, h=4))
+    batch = fl.DeviceBatch(det, W, H, 3)
+    d = torch.from_numpy(frames).cuda()
+    batch.run_device(d.data_ptr(), W * H, W, 3)
+    torch.cuda.synchronize()
+    for k in range(1, L):
+        base, w, h, pitch, fs = batch.pyramid_level(k)
+        host = read_device(base, 2 * fs + pitch * h)
+        for f in range(3):
+            lvl = host[f * fs:f * fs + pitch * h].reshape(h, pitch)[:, :w]
+            assert (lvl == orc.pyramid(frames[f], L)[k]).all()
+
+
+def test_device_synth_matches_host_generator():
+    import torch
+    W, H, n = 752, 480, 3
+    for kind, fn in ((0, synth.noise), (1, synth.texture)):
+        d = torch.zeros((n, H, W), dtype=torch.uint8, device="cuda")
+        fl.synth_frames_device(d.data_ptr(), kind, 7, n, W, H, W, W * H)
+        torch.cuda.synchronize()
+        got = d.cpu().numpy()
+        for f in range(n):
+            assert (got[f] == fn(7 + f, W, H)).all()
+
+
+def test_device_batch_equals_single_frame_runs(orc):
+    import torch
+    W, H, n = 752, 480, 40
+    cfg = dict(epsilon=10, N=9, score_kind="sad_b", l=3, w=1, h=8, n=1)
+    det = fl.Detector(make_config(cfg))
+    batch = fl.DeviceBatch(det, W, H, n)
+    pitch = 768
+    d = torch.zeros((n, H, pitch), dtype=torch.uint8, device="cuda")
+    fl.synth_frames_device(d.data_ptr(), 1, 100, n, W, H, pitch, pitch * H)
+    batch.run_device(d.data_ptr(), pitch * H, pitch, n)
+    torch.cuda.synchronize()
+    res = batch.results(n)
+    p = oracle.make_params(**cfg)
+    for f in (0, 1, 17, n - 1):
+        ref, _ = orc.detect(synth.texture(100 + f, W, H), p)
+        assert (res[f] == ref).all()
+    # host-fed path through flkb_batch_run_host (pinned host buffer)
+    host = d[:, :, :W].contiguous().cpu().pin_memory()
+    batch2 = fl.DeviceBatch(det, W, H, n)
+    batch2.run_host(host.data_ptr(), W * H, W, n)
+    torch.cuda.synchronize()
+    res2 = batch2.results(n)
+    assert all((a == b).all() for a, b in zip(res, res2))
+    # host batch API over flk_image handles
+    frames = [synth.texture(100 + f, W, H) for f in range(10)]
+    out = det.run_batch(frames)
+    assert all((a == b).all() for a, b in zip(out, res[:10]))
+
+
+def test_conformance_tally_matches_reference_semantics(orc):
+    img = synth.texture(10, 256, 192)
+    cfg = dict(epsilon=10, N=10, score_kind="sad_b", l=2, w=1, h=16, n=1)
+    det = fl.Detector(make_config(cfg))
+    feats, extra = det.run(img, stats=True, conformance=True)
+    conf = extra["conformance"]
+    want = orc.conformance(img, oracle.make_params(**cfg), feats)
+    assert (conf["matched"], conf["subset_only"], conf["false_positives"]) == (
+        want.matched, want.subset_only, want.false_positives)
+    assert conf["false_positives"] == 0 and conf["matched"] == len(feats)
+    cells = {(f["cell_x"], f["cell_y"]) for f in feats}
+    assert len(cells) == len(feats) and (feats["score"] > 0).all()
+
+
+def test_errors_through_the_abi():
+    det = fl.Detector(fl.Config(l=2, h=16))
+    det.run(synth.texture(10, 256, 192))
+    with pytest.raises(fl.DimensionMismatch):
+        det.run(synth.texture(11, 128, 96))
+    with pytest.raises(fl.InvalidArgument):
+        fl.Detector(fl.Config(l=3)).run(synth.noise(3, 32, 20))  # 8x5 at level 2
+
+
+def test_repeatable_and_launch_counted():
+    img = synth.noise(3, 752, 480)
+    det = fl.Detector(fl.Config(N=9, l=3, h=8))
+    before = fl.kernel_launch_count()
+    a = det.run(img)
+    b = det.run(img)
+    assert (a == b).all()
+    assert fl.kernel_launch_count() > before
