@@ -285,7 +285,7 @@ def main():
         }
         if not args.no_cpu_baseline and world == 1:
             workers = os.cpu_count() or 1
-            line["cpu_baseline"] = cpu_reference(min(2048, max(256, 16 * workers)), workers)
+            line["cpu_baseline"] = cpu_reference(min(4096, max(512, 128 * workers)), workers)
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

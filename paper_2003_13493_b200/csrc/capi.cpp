@@ -138,7 +138,7 @@ class FrameRunner {
     flkb::DeviceGuard guard(device_);
     std::memcpy(in_.p, img.px.data(), img.px.size());
     enqueue_copy_in();
-    batch_.run(d_in_, static_cast<size_t>(pitch_) * h_, pitch_, 1, false, stream_);
+    batch_.run_staged(d_in_, static_cast<size_t>(pitch_) * h_, pitch_, 1, false, stream_);
     batch_.download_responses(0, out, stream_);
   }
 
@@ -576,6 +576,8 @@ flk_status flkb_batch_run_host(flkb_batch* b, const uint8_t* frames, size_t fram
       throw flkb::InvalidArgument("host frame layout smaller than the frame size");
     flkb::DeviceGuard guard(b->device);
     if (!b->d_in) {
+      // frames stay densely packed when the width is already 16-B aligned, so
+      // the H2D copy is one linear transfer
       b->in_pitch = static_cast<int>(round16(static_cast<size_t>(g.width)));
       b->in_stride = static_cast<size_t>(b->in_pitch) * g.height;
       flkb::check_cuda(cudaMalloc(&b->d_in, b->in_stride * db.capacity() + 16), "batch input");
@@ -594,7 +596,10 @@ flk_status flkb_batch_run_host(flkb_batch* b, const uint8_t* frames, size_t fram
       cudaStream_t s = b->side[si];
       uint8_t* dst = b->d_in + static_cast<size_t>(c0) * b->in_stride;
       const uint8_t* src = frames + static_cast<size_t>(c0) * frame_stride;
-      if (frame_stride == static_cast<size_t>(row_pitch) * g.height) {
+      if (row_pitch == b->in_pitch && frame_stride == b->in_stride) {
+        flkb::check_cuda(cudaMemcpyAsync(dst, src, b->in_stride * cnt, cudaMemcpyHostToDevice, s),
+                         "H2D frames");
+      } else if (frame_stride == static_cast<size_t>(row_pitch) * g.height) {
         flkb::check_cuda(cudaMemcpy2DAsync(dst, b->in_pitch, src, row_pitch, g.width,
                                            static_cast<size_t>(g.height) * cnt,
                                            cudaMemcpyHostToDevice, s), "H2D frames");

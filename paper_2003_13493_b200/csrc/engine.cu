@@ -8,6 +8,7 @@
 
 #include "conformance.cuh"
 #include "engine.hpp"
+#include "kernels_fused.cuh"
 #include "kernels_v1.cuh"
 
 namespace flkb {
@@ -148,10 +149,163 @@ DeviceBatch::~DeviceBatch() {
   if (cur >= 0) cudaSetDevice(cur);
 }
 
-int DeviceBatch::kernels_per_run() const { return 3 * g_.levels; }
+int DeviceBatch::kernels_per_run() const { return g_.levels + 1; }
+
+namespace {
+
+using FusedFn = void (*)(const fused::Params);
+
+template <int N>
+FusedFn fused_for_kind(int kind) {
+  switch (kind) {
+    case kSadB: return fused::k_detect<N, kSadB>;
+    case kSadA: return fused::k_detect<N, kSadA>;
+    default: return fused::k_detect<N, kMt>;
+  }
+}
+
+FusedFn fused_kernel(int n, int kind) {
+  switch (n) {
+    case 9: return fused_for_kind<9>(kind);
+    case 10: return fused_for_kind<10>(kind);
+    case 11: return fused_for_kind<11>(kind);
+    case 12: return fused_for_kind<12>(kind);
+    case 13: return fused_for_kind<13>(kind);
+    case 14: return fused_for_kind<14>(kind);
+    case 15: return fused_for_kind<15>(kind);
+    default: return fused_for_kind<16>(kind);
+  }
+}
+
+constexpr int kFusedSmemTarget = 112 * 1024;  // two CTAs per SM
+constexpr int kFusedSmemMax = 227 * 1024;
+
+// Shared-memory geometry of the fused kernel for column tiles of at most
+// `tile_w` pixels (every level uses the same layout).
+fused::Params fused_geometry(const DetectParams& p, const Geometry& g, int R, int tiles0) {
+  fused::Params P{};
+  P.levels = g.levels;
+  P.eps = p.epsilon;
+  P.radius = p.radius;
+  P.R = R;
+  P.cell_w = p.cell_w;
+  P.cell_h = p.cell_h;
+  P.cols = g.cols;
+  P.cells = g.cells;
+  const int n = p.radius;
+  int tw_max = 1, slots = 0, cta = 0;
+  for (int k = 0; k < g.levels; ++k) {
+    fused::Level& L = P.lv[k];
+    L.w = g.lw[k];
+    L.h = g.lh[k];
+    L.tiles_x = std::max(1, std::min(tiles0, (L.w + 63) / 64));
+    L.tile_w = (L.w + L.tiles_x - 1) / L.tiles_x;
+    L.tiles_x = (L.w + L.tile_w - 1) / L.tile_w;
+    L.bands = (L.h + R - 1) / R;
+    L.cta0 = cta;
+    cta += L.bands * L.tiles_x;
+    tw_max = std::max(tw_max, L.tile_w);
+    slots = std::max(slots, ((R << k) / p.cell_h + 2) * g.cols);
+  }
+  P.nw_max = (tw_max + 2 * n + 15 + fused::kOwn - 1) / fused::kOwn;
+  P.sw = static_cast<int>(round_up(
+      static_cast<size_t>(std::max(fused::kOwn * (P.nw_max - 1) + 36, tw_max + 2 * n + 22)), 16));
+  P.rp = static_cast<int>(round_up(static_cast<size_t>(tw_max + 4 * n), 8));
+  // 32-bit in-cell keys need cells of at most 1024 px per side
+  P.key_slots = (p.cell_w <= 1024 && p.cell_h <= 1024 && slots <= 4096) ? slots : 0;
+  return P;
+}
+
+}  // namespace
 
 void DeviceBatch::run(const uint8_t* frames, size_t fstride, int pitch, int count, bool stats,
                       cudaStream_t s, StageTimes* times, int first) {
+  if (count < 1 || first < 0 || first + count > capacity_)
+    throw InvalidArgument("batch count " + std::to_string(count) + " outside [1, " +
+                          std::to_string(capacity_) + "]");
+  if (pitch < g_.width) throw InvalidArgument("row pitch smaller than the frame width");
+  if (count > 65535) throw InvalidArgument("at most 65535 frames per launch");
+  DeviceGuard guard(device_);
+  const int R = fused_R_;
+  int tiles0 = 1;
+  fused::Params P = fused_geometry(p_, g_, R, tiles0);
+  while (fused::smem_layout(P).total > kFusedSmemTarget && P.lv[0].tile_w > 64) {
+    ++tiles0;
+    P = fused_geometry(p_, g_, R, tiles0);
+  }
+  const int smem = fused::smem_layout(P).total;
+  if (smem > kFusedSmemMax) {  // pathological radius / geometry: staged kernels
+    run_staged(frames, fstride, pitch, count, stats, s, times, first);
+    return;
+  }
+  const FusedFn kern = fused_kernel(p_.arc_length, p_.score);
+  if (static_cast<size_t>(smem) > fused_smem_) {
+    check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
+               "fused smem attribute");
+    fused_smem_ = static_cast<size_t>(smem);
+  }
+  uint8_t* pyr = d_pyr_ ? d_pyr_ + static_cast<size_t>(first) * g_.pyr_frame_bytes : nullptr;
+  unsigned long long* keys = d_keys_ + static_cast<size_t>(first) * g_.cells;
+  flk_feature* feats = d_feats_ + static_cast<size_t>(first) * g_.cells;
+  int* counts = d_counts_ + first;
+  unsigned long long* st =
+      reinterpret_cast<unsigned long long*>(d_stats_ + 2 * static_cast<size_t>(first));
+
+  cudaEvent_t ev[4] = {};
+  if (times) {
+    for (auto& e : ev) check_cuda(cudaEventCreate(&e), "cudaEventCreate");
+    check_cuda(cudaEventRecord(ev[0], s), "cudaEventRecord");
+  }
+  if (stats) check_cuda(cudaMemsetAsync(st, 0, sizeof(uint64_t) * 2 * count, s), "memset stats");
+  int launched = 0;
+  for (int k = 1; k < g_.levels; ++k) {
+    const uint8_t* src = k == 1 ? frames : pyr + g_.loff[k - 1];
+    const int sp = k == 1 ? pitch : g_.lpitch[k - 1];
+    const size_t sfs = k == 1 ? fstride : g_.pyr_frame_bytes;
+    const int vec_ok = (reinterpret_cast<uintptr_t>(src) % 16 == 0) && sp % 16 == 0 && sfs % 16 == 0;
+    dim3 block(32, 8), grid((g_.lw[k] + 255) / 256, (g_.lh[k] + 7) / 8, count);
+    k_pyramid_down<<<grid, block, 0, s>>>(src, sp, sfs, pyr + g_.loff[k], g_.lpitch[k],
+                                          g_.pyr_frame_bytes, g_.lw[k], g_.lh[k], vec_ok);
+    ++launched;
+  }
+  if (times) check_cuda(cudaEventRecord(ev[1], s), "cudaEventRecord");
+  int ctas = 0;
+  for (int k = 0; k < g_.levels; ++k) {
+    fused::Level& L = P.lv[k];
+    L.img = k == 0 ? frames : pyr + g_.loff[k];
+    L.pitch = k == 0 ? pitch : g_.lpitch[k];
+    L.fstride = k == 0 ? fstride : g_.pyr_frame_bytes;
+    L.tma = (reinterpret_cast<uintptr_t>(L.img) % 16 == 0) && L.pitch % 16 == 0 &&
+            L.fstride % 16 == 0;
+    ctas += L.bands * L.tiles_x;
+  }
+  P.keys = keys;
+  P.stats = stats ? st : nullptr;
+  kern<<<dim3(ctas, count), fused::kThreads, smem, s>>>(P);
+  ++launched;
+  if (times) check_cuda(cudaEventRecord(ev[2], s), "cudaEventRecord");
+  k_compact<<<count, 256, 0, s>>>(keys, g_.cols, g_.cells, feats, counts);
+  ++launched;
+  check_cuda(cudaGetLastError(), "kernel launch");
+  count_launches(launched);
+  if (times) {
+    check_cuda(cudaEventRecord(ev[3], s), "cudaEventRecord");
+    check_cuda(cudaEventSynchronize(ev[3]), "cudaEventSynchronize");
+    float a = 0, b = 0, c = 0;
+    cudaEventElapsedTime(&a, ev[0], ev[1]);
+    cudaEventElapsedTime(&b, ev[1], ev[2]);
+    cudaEventElapsedTime(&c, ev[2], ev[3]);
+    // the fused kernel computes responses and suppression together: its time
+    // is reported as crf_us; nms_us is the cell compaction
+    times->pyramid_us = a * 1e3;
+    times->crf_us = b * 1e3;
+    times->nms_us = c * 1e3;
+    for (auto& e : ev) cudaEventDestroy(e);
+  }
+}
+
+void DeviceBatch::run_staged(const uint8_t* frames, size_t fstride, int pitch, int count,
+                             bool stats, cudaStream_t s, StageTimes* times, int first) {
   if (count < 1 || first < 0 || first + count > capacity_)
     throw InvalidArgument("batch count " + std::to_string(count) + " outside [1, " +
                           std::to_string(capacity_) + "]");

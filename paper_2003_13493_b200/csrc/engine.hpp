@@ -77,6 +77,10 @@ class DeviceBatch {
   // call synchronizes and reports per-stage device time.
   void run(const uint8_t* frames, size_t frame_stride, int pitch, int count, bool stats,
            cudaStream_t stream, StageTimes* times = nullptr, int first = 0);
+  // The staged pipeline (one launch per stage and level, u16 score maps in
+  // HBM): the diagnostic path behind download_responses().
+  void run_staged(const uint8_t* frames, size_t frame_stride, int pitch, int count, bool stats,
+                  cudaStream_t stream, StageTimes* times = nullptr, int first = 0);
   void download(int first, int count, int* counts, flk_feature* feats, cudaStream_t s) const;
   // Score maps of frame `frame` of the last run, every level, tightly packed
   // floats (the reference's ResponseMap values). Synchronous.
@@ -110,6 +114,9 @@ class DeviceBatch {
   int* d_counts_ = nullptr;
   uint64_t* d_stats_ = nullptr;  // [capacity][2] = candidates, comparisons
   float* d_naive_ = nullptr;     // conformance scratch (lazily allocated)
+  size_t fused_smem_ = 0;        // dynamic shared memory of the fused kernel
+  int fused_R_ = 32;             // rows per band
+  int fused_tile_w_[kMaxLevels] = {};
   int* d_conf_ = nullptr;
 };
 

@@ -1,0 +1,556 @@
+// Fused FAST + score + window-max suppression + cell selection, one CTA per
+// (frame, level, band of rows, column tile). sm_100a.
+//
+//  1. TMA   cp.async.bulk copies the tile's image rows (+3+n halo) of level k
+//           from HBM into shared memory, completion on an mbarrier.
+//  2. SLICE every 32-byte window (stride 26 px) is transposed into 8 bit
+//           planes: bit b of plane k = bit k of pixel x0+b. A word "owns"
+//           its middle 26 pixels, so every ring offset (|dx| <= 3) stays
+//           inside the word -- no neighbour exchange.
+//  3. MASKS bit-sliced FAST: per word, thresholds L = sat(c-eps) and
+//           H = sat(c+eps) as 8 planes each, then for each of the 16 ring
+//           positions the shifted ring planes are compared with a borrow
+//           chain (one LOP3 per bit): dark_i = R_i < L, bright_i = H < R_i,
+//           32 pixels per instruction. The segment test is a bit-sliced
+//           sliding AND over the 16 position words (runs of 3, then 9, then
+//           N) -- 32 pixels' corner decisions per LOP3. Identical to the
+//           reference LUT test (fast.cpp:34-65, 221-247).
+//  4. SCORE corners are compacted per warp (popc + shuffle scan) and scored
+//           one per lane: SAD-B through VABSDIFF4 on packed ring bytes,
+//           SAD-A / MT through the register formulations of fast_math.cuh.
+//           Scores land in a zero-padded u16 tile in shared memory.
+//  5. NMS   each candidate in the band's own rows is tested against its
+//           (2n+1)^2 window with spiral_is_local_max's tie rule
+//           (nms.cpp:48-79); survivors update a 32-bit per-cell key in
+//           shared memory with one ATOMS.MAX (score, -y, -x inside the cell;
+//           the level is fixed per CTA).
+//  6. FLUSH each non-empty cell key becomes the global u64 key (score,
+//           -level, -y0, -x0) via one atomicMax -- the cross-level
+//           cell_candidate_wins order (nms.cpp:41-46).
+#pragma once
+
+#include <cstdint>
+
+#include "fast_math.cuh"
+
+namespace flkb {
+namespace fused {
+
+constexpr int kOwn = 26;       // pixels owned by one 32-bit plane word
+constexpr int kThreads = 256;
+constexpr int kWarps = kThreads / 32;
+constexpr int kMaxLv = 16;
+
+struct Level {
+  const uint8_t* img;  // frame 0, row 0
+  size_t fstride;
+  int pitch, w, h;
+  int tiles_x, tile_w;  // column tiles and NMS columns per tile
+  int bands;            // row bands of R rows
+  int cta0;             // first blockIdx.x of this level
+  int tma;              // rows may be fetched with cp.async.bulk
+};
+
+struct Params {
+  Level lv[kMaxLv];
+  int levels;
+  int eps, radius, R;
+  int cell_w, cell_h, cols, cells;
+  int sw;         // stage row pitch (bytes)
+  int nw_max;     // plane words per row, max over tiles
+  int rp;         // score tile pitch (u16)
+  int key_slots;  // shared cell-key capacity
+  unsigned long long* keys;
+  unsigned long long* stats;
+};
+
+struct Smem {
+  int stage, planes, cm, lists, skeys, bar, total;
+};
+
+__host__ __device__ inline Smem smem_layout(const Params& p) {
+  const int img_rows = p.R + 2 * p.radius + 6;
+  const int fast_rows = p.R + 2 * p.radius;
+  Smem s;
+  int off = 0;
+  s.stage = off;
+  off += img_rows * p.sw;
+  off = (off + 127) & ~127;
+  s.planes = off;  // aliased by the score tile after the mask phase
+  const int pl = img_rows * p.nw_max * 32;
+  const int rt = fast_rows * p.rp * 2;
+  off += pl > rt ? pl : rt;
+  off = (off + 127) & ~127;
+  s.cm = off;
+  off += fast_rows * p.nw_max * 4;
+  off = (off + 15) & ~15;
+  s.lists = off;
+  off += kWarps * 32 * kOwn * 2;
+  off = (off + 15) & ~15;
+  s.skeys = off;
+  off += p.key_slots * 4;
+  off = (off + 15) & ~15;
+  s.bar = off;
+  off += 16;
+  s.total = off;
+  return s;
+}
+
+// ------------------------------------------------------------ primitives
+
+__device__ __forceinline__ uint32_t lop3_maj_na(uint32_t a, uint32_t b, uint32_t c) {
+  uint32_t d;  // (~a & b) | (~a & c) | (b & c): borrow of a - b - c
+  asm("lop3.b32 %0, %1, %2, %3, 0x8E;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+  return d;
+}
+__device__ __forceinline__ uint32_t lop3_maj(uint32_t a, uint32_t b, uint32_t c) {
+  uint32_t d;
+  asm("lop3.b32 %0, %1, %2, %3, 0xE8;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+  return d;
+}
+__device__ __forceinline__ uint32_t lop3_xor3(uint32_t a, uint32_t b, uint32_t c) {
+  uint32_t d;
+  asm("lop3.b32 %0, %1, %2, %3, 0x96;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+  return d;
+}
+__device__ __forceinline__ uint32_t and3(uint32_t a, uint32_t b, uint32_t c) { return a & b & c; }
+__device__ __forceinline__ uint32_t or3(uint32_t a, uint32_t b, uint32_t c) { return a | b | c; }
+
+// Bit-sliced unsigned a < b over 8 planes (plane 0 = LSB): borrow out of a - b.
+__device__ __forceinline__ uint32_t sliced_less(const uint32_t (&a)[8], const uint32_t (&b)[8]) {
+  uint32_t br = ~a[0] & b[0];
+#pragma unroll
+  for (int k = 1; k < 8; ++k) br = lop3_maj_na(a[k], b[k], br);
+  return br;
+}
+
+// 32 pixels (8 words, pixel 4m+i in byte i of word m) -> 8 bit planes.
+__device__ __forceinline__ void transpose32x8(const uint32_t (&w)[8], uint32_t (&p)[8]) {
+  uint32_t lo[4], hi[4];
+#pragma unroll
+  for (int t = 0; t < 4; ++t) {
+    uint32_t l = w[2 * t], h = w[2 * t + 1], x;
+    x = (l ^ (l >> 7)) & 0x00AA00AAu;
+    l = l ^ x ^ (x << 7);
+    x = (h ^ (h >> 7)) & 0x00AA00AAu;
+    h = h ^ x ^ (x << 7);
+    x = (l ^ (l >> 14)) & 0x0000CCCCu;
+    l = l ^ x ^ (x << 14);
+    x = (h ^ (h >> 14)) & 0x0000CCCCu;
+    h = h ^ x ^ (x << 14);
+    x = (l ^ (h << 4)) & 0xF0F0F0F0u;
+    l ^= x;
+    h ^= x >> 4;
+    lo[t] = l;
+    hi[t] = h;
+  }
+  // 4x4 byte transposes: plane k byte t = block t byte k
+  uint32_t a = __byte_perm(lo[0], lo[1], 0x5140), b = __byte_perm(lo[0], lo[1], 0x7362);
+  uint32_t c = __byte_perm(lo[2], lo[3], 0x5140), d = __byte_perm(lo[2], lo[3], 0x7362);
+  p[0] = __byte_perm(a, c, 0x5410);
+  p[1] = __byte_perm(a, c, 0x7632);
+  p[2] = __byte_perm(b, d, 0x5410);
+  p[3] = __byte_perm(b, d, 0x7632);
+  a = __byte_perm(hi[0], hi[1], 0x5140);
+  b = __byte_perm(hi[0], hi[1], 0x7362);
+  c = __byte_perm(hi[2], hi[3], 0x5140);
+  d = __byte_perm(hi[2], hi[3], 0x7362);
+  p[4] = __byte_perm(a, c, 0x5410);
+  p[5] = __byte_perm(a, c, 0x7632);
+  p[6] = __byte_perm(b, d, 0x5410);
+  p[7] = __byte_perm(b, d, 0x7632);
+}
+
+// Bit-sliced segment test: some cyclic run of >= N set positions among the
+// 16 position words (bit lanes = pixels).
+template <int N>
+__device__ __forceinline__ uint32_t sliced_arc(const uint32_t (&m)[16]) {
+  uint32_t w3[16], w9[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) w3[i] = and3(m[i], m[(i + 1) & 15], m[(i + 2) & 15]);
+#pragma unroll
+  for (int i = 0; i < 16; ++i) w9[i] = and3(w3[i], w3[(i + 3) & 15], w3[(i + 6) & 15]);
+  if (N > 9) {
+#pragma unroll
+    for (int i = 0; i < 16; ++i) w3[i] = w9[i] & w9[(i + N - 9) & 15];
+  } else {
+#pragma unroll
+    for (int i = 0; i < 16; ++i) w3[i] = w9[i];
+  }
+  uint32_t a = or3(w3[0], w3[1], w3[2]), b = or3(w3[3], w3[4], w3[5]);
+  uint32_t c = or3(w3[6], w3[7], w3[8]), d = or3(w3[9], w3[10], w3[11]);
+  uint32_t e = or3(w3[12], w3[13], w3[14]);
+  return or3(or3(a, b, c), or3(d, e, w3[15]), 0u);
+}
+
+__device__ __forceinline__ uint32_t vabsdiff4_acc(uint32_t a, uint32_t b, uint32_t acc) {
+  uint32_t d;
+  asm("vabsdiff4.u32.u32.u32.add %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(acc));
+  return d;
+}
+
+// SAD-B of one corner from its 16 ring bytes packed 4 per word:
+// sum max(|d|-e,0) = (sum | |d| - e | + sum |d| - 16 e) / 2.
+__device__ __forceinline__ int sad_b_packed(const uint32_t (&r)[4], uint32_t c, uint32_t eps) {
+  const uint32_t c4 = c * 0x01010101u, e4 = eps * 0x01010101u;
+  uint32_t acc1 = 0, acc2 = 0;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const uint32_t d = __vabsdiffu4(r[k], c4);
+    acc1 = vabsdiff4_acc(d, e4, acc1);
+    acc2 = vabsdiff4_acc(r[k], c4, acc2);
+  }
+  return static_cast<int>((acc1 + acc2 - 16u * eps) >> 1);
+}
+
+// ---------------------------------------------------------------- kernel
+
+template <int N, int KIND>
+__global__ void __launch_bounds__(kThreads, 2) k_detect(const __grid_constant__ Params P) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  const Smem S = smem_layout(P);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+
+  // --- which level, band and column tile
+  int k = 0;
+  while (k + 1 < P.levels && static_cast<int>(blockIdx.x) >= P.lv[k + 1].cta0) ++k;
+  const Level& L = P.lv[k];
+  const int local = blockIdx.x - L.cta0;
+  const int band = local / L.tiles_x, tile = local % L.tiles_x;
+  const int f = blockIdx.y;
+  const int n = P.radius, w = L.w, h = L.h;
+  const int y0 = band * P.R, y1 = min(y0 + P.R, h);          // rows suppressed here
+  const int x_lo = tile * L.tile_w, x_hi = min(x_lo + L.tile_w, w);
+  const int fy0 = y0 - n;                                       // tile row 0 <-> image row fy0
+  const int iy0 = fy0 - 3;                                      // stage row 0 <-> image row iy0
+  const int ya = max(iy0, 0), yb = min(y1 + n + 3, h);          // rows present in the stage
+  const int bx0 = (x_lo - n - 3) & ~15;                         // stage column 0 <-> image x bx0
+  const int nw = (x_hi + n - bx0 - 3 + kOwn - 1) / kOwn;        // plane words per row
+  const int cx_lo = max(x_lo - n, 3), cx_hi = min(x_hi + n, w - 3);  // FAST columns
+  const int cy_lo = max(fy0, 3), cy_hi = min(y1 + n, h - 3);         // FAST rows
+
+  uint8_t* stage = smem + S.stage;
+  uint32_t* planes = reinterpret_cast<uint32_t*>(smem + S.planes);
+  uint16_t* tile_s = reinterpret_cast<uint16_t*>(smem + S.planes);
+  uint32_t* cm = reinterpret_cast<uint32_t*>(smem + S.cm);
+  uint16_t* lists = reinterpret_cast<uint16_t*>(smem + S.lists) + warp * (32 * kOwn);
+  uint32_t* skeys = reinterpret_cast<uint32_t*>(smem + S.skeys);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + S.bar);
+
+  // cell rows touched by the suppressed rows [y0, y1) of level k
+  const int cr0 = (y0 << k) / P.cell_h;
+  const int cr1 = y1 > y0 ? ((y1 - 1) << k) / P.cell_h : cr0;
+  const int slots = (cr1 - cr0 + 1) * P.cols;
+  const bool local_keys = slots <= P.key_slots;
+
+  // --- 1. stage the rows [ya, yb), columns [max(bx0,0), ...) of this tile
+  const uint8_t* frame = L.img + f * L.fstride;
+  const int gx0 = max(bx0, 0);
+  const int sx0 = gx0 - bx0;  // multiple of 16
+  int row_bytes = min(bx0 + P.sw, L.pitch) - gx0;
+  row_bytes = min(row_bytes, ((w + 15) & ~15) - gx0);
+  if (L.tma) {
+    row_bytes &= ~15;
+    if (tid == 0) {
+      const uint32_t b = static_cast<uint32_t>(__cvta_generic_to_shared(bar));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(b));
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      const uint32_t bytes = static_cast<uint32_t>(row_bytes * (yb - ya));
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(bytes)
+                   : "memory");
+      for (int y = ya; y < yb; ++y) {
+        const uint32_t dst = static_cast<uint32_t>(
+            __cvta_generic_to_shared(stage + (y - iy0) * P.sw + sx0));
+        const uint8_t* src = frame + static_cast<size_t>(y) * L.pitch + gx0;
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+                "r"(dst), "l"(src), "r"(row_bytes), "r"(b)
+            : "memory");
+      }
+    }
+  } else {
+    for (int i = tid; i < (yb - ya) * row_bytes; i += kThreads) {
+      const int y = ya + i / row_bytes, x = i % row_bytes;
+      stage[(y - iy0) * P.sw + sx0 + x] = frame[static_cast<size_t>(y) * L.pitch + gx0 + x];
+    }
+  }
+  if (local_keys)
+    for (int i = tid; i < slots; i += kThreads) skeys[i] = 0u;
+  __syncthreads();
+  if (L.tma) {
+    const uint32_t b = static_cast<uint32_t>(__cvta_generic_to_shared(bar));
+    uint32_t done = 0;
+    while (!done) {
+      asm volatile(
+          "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0; selp.u32 %0, 1, 0, p; }"
+          : "=r"(done)
+          : "r"(b)
+          : "memory");
+    }
+  }
+
+  // --- 2. bit planes of every staged row
+  {
+    const int tasks = (yb - ya) * nw;
+    for (int t = tid; t < tasks; t += kThreads) {
+      const int r = ya - iy0 + t / nw, j = t % nw;
+      const int bx = kOwn * j;
+      const uint32_t* src = reinterpret_cast<const uint32_t*>(stage + r * P.sw + (bx & ~3));
+      uint32_t a[9], wv[8], pl[8];
+#pragma unroll
+      for (int i = 0; i < 9; ++i) a[i] = src[i];
+      const uint32_t sel = (bx & 2) ? 0x5432u : 0x3210u;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) wv[i] = __byte_perm(a[i], a[i + 1], sel);
+      transpose32x8(wv, pl);
+      uint4* dst = reinterpret_cast<uint4*>(planes + (r * P.nw_max + j) * 8);
+      dst[0] = make_uint4(pl[0], pl[1], pl[2], pl[3]);
+      dst[1] = make_uint4(pl[4], pl[5], pl[6], pl[7]);
+    }
+  }
+  __syncthreads();
+
+  // --- 3. bit-sliced corner masks for the FAST rows
+  const int fast_rows = cy_hi - cy_lo;
+  {
+    uint32_t E[8];
+#pragma unroll
+    for (int b = 0; b < 8; ++b) E[b] = ((P.eps >> b) & 1) ? 0xFFFFFFFFu : 0u;
+    const int tasks = max(fast_rows, 0) * nw;
+    for (int t = tid; t < tasks; t += kThreads) {
+      const int y = cy_lo + t / nw, j = t % nw;
+      const int r = y - iy0;  // stage/plane row of the centre
+      const uint32_t* base = planes + j * 8;
+      auto row_planes = [&](int rr, uint32_t (&q)[8]) {
+        const uint4* s4 = reinterpret_cast<const uint4*>(base + rr * P.nw_max * 8);
+        const uint4 u = s4[0], v = s4[1];
+        q[0] = u.x; q[1] = u.y; q[2] = u.z; q[3] = u.w;
+        q[4] = v.x; q[5] = v.y; q[6] = v.z; q[7] = v.w;
+      };
+      uint32_t c[8], lo[8], hi[8];
+      row_planes(r, c);
+      {
+        uint32_t br = 0, cy = 0;
+#pragma unroll
+        for (int b = 0; b < 8; ++b) {
+          lo[b] = lop3_xor3(c[b], E[b], br);
+          br = lop3_maj_na(c[b], E[b], br);
+          hi[b] = lop3_xor3(c[b], E[b], cy);
+          cy = lop3_maj(c[b], E[b], cy);
+        }
+#pragma unroll
+        for (int b = 0; b < 8; ++b) {
+          lo[b] &= ~br;  // c - eps < 0  -> 0
+          hi[b] |= cy;   // c + eps > 255 -> 255
+        }
+      }
+      uint32_t dk[16], bk[16];
+#pragma unroll
+      for (int dy = -3; dy <= 3; ++dy) {
+        uint32_t q[8];
+        row_planes(r + dy, q);
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          if (ring_dy(i) != dy) continue;
+          const int dx = ring_dx(i);
+          uint32_t s[8];
+#pragma unroll
+          for (int b = 0; b < 8; ++b) s[b] = dx > 0 ? (q[b] >> dx) : dx < 0 ? (q[b] << -dx) : q[b];
+          dk[i] = sliced_less(s, lo);
+          bk[i] = sliced_less(hi, s);
+        }
+      }
+      uint32_t corner = sliced_arc<N>(dk) | sliced_arc<N>(bk);
+      // owned bits [3, 29) that fall inside the FAST columns
+      const int xb = bx0 + kOwn * j;
+      const int lo_b = max(3, cx_lo - xb), hi_b = min(29, cx_hi - xb);
+      const uint32_t valid = hi_b > lo_b ? ((hi_b >= 32 ? 0xFFFFFFFFu : ((1u << hi_b) - 1u)) &
+                                            ~((1u << lo_b) - 1u))
+                                         : 0u;
+      cm[(y - cy_lo) * nw + j] = corner & valid;
+    }
+  }
+  __syncthreads();
+
+  // --- 4. zero the score tile (aliases the planes), then score corners
+  const int tile_rows = P.R + 2 * n;
+  {
+    uint4* z = reinterpret_cast<uint4*>(tile_s);
+    const int n16 = (tile_rows * P.rp * 2) / 16;
+    for (int i = tid; i < n16; i += kThreads) z[i] = make_uint4(0, 0, 0, 0);
+  }
+  __syncthreads();
+  // tile column of image x: x - (x_lo - n) + n  (left zero margin of n)
+  const int tx0 = x_lo - 2 * n;
+  auto stage_px = [&](int y, int x) -> uint32_t { return stage[(y - iy0) * P.sw + (x - bx0)]; };
+  {
+    const int tasks = max(fast_rows, 0) * nw;
+    for (int c0 = warp * 32; c0 < tasks; c0 += kThreads) {
+      const int t = c0 + lane;
+      uint32_t m = t < tasks ? cm[t] : 0u;
+      const int cnt = __popc(m);
+      int incl = cnt;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += v;
+      }
+      const int total = __shfl_sync(0xffffffffu, incl, 31);
+      int pos = incl - cnt;
+      while (m) {
+        const int b = __ffs(m) - 1;
+        m &= m - 1;
+        lists[pos++] = static_cast<uint16_t>((lane << 5) | b);
+      }
+      __syncwarp();
+      for (int e = lane; e < total; e += 32) {
+        const int ent = lists[e];
+        const int tt = c0 + (ent >> 5);
+        const int y = cy_lo + tt / nw, j = tt % nw;
+        const int x = bx0 + kOwn * j + (ent & 31);
+        const uint32_t cc = stage_px(y, x);
+        int s;
+        if (KIND == kSadB) {
+          uint32_t rb[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) rb[i] = stage_px(y + ring_dy(i), x + ring_dx(i));
+          uint32_t pk[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            pk[q] = __byte_perm(__byte_perm(rb[4 * q], rb[4 * q + 1], 0x0040),
+                                __byte_perm(rb[4 * q + 2], rb[4 * q + 3], 0x0040), 0x5410);
+          s = sad_b_packed(pk, cc, static_cast<uint32_t>(P.eps));
+        } else {
+          int ring[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) ring[i] = stage_px(y + ring_dy(i), x + ring_dx(i));
+          s = fast_score<N, KIND>(static_cast<int>(cc), ring, P.eps);
+        }
+        tile_s[(y - fy0) * P.rp + (x - tx0)] = static_cast<uint16_t>(s);
+      }
+      __syncwarp();
+    }
+  }
+  __syncthreads();
+
+  // --- 5. suppression + per-cell keys for candidates in rows [y0, y1)
+  unsigned long long n_cand = 0, n_cmp = 0;
+  {
+    const int ny_lo = max(y0, 3), ny_hi = min(y1, h - 3);
+    const int nx_lo = max(x_lo, 3), nx_hi = min(x_hi, w - 3);
+    const int row_off = ny_lo - cy_lo;
+    const int tasks = max(ny_hi - ny_lo, 0) * nw;
+    for (int c0 = warp * 32; c0 < tasks; c0 += kThreads) {
+      const int t = c0 + lane;
+      uint32_t m = 0;
+      if (t < tasks) {
+        const int j = t % nw;
+        const int xb = bx0 + kOwn * j;
+        const int lo_b = max(3, nx_lo - xb), hi_b = min(29, nx_hi - xb);
+        const uint32_t own = hi_b > lo_b ? ((hi_b >= 32 ? 0xFFFFFFFFu : ((1u << hi_b) - 1u)) &
+                                            ~((1u << lo_b) - 1u))
+                                         : 0u;
+        m = cm[(row_off + t / nw) * nw + j] & own;
+      }
+      const int cnt = __popc(m);
+      int incl = cnt;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += v;
+      }
+      const int total = __shfl_sync(0xffffffffu, incl, 31);
+      int pos = incl - cnt;
+      while (m) {
+        const int b = __ffs(m) - 1;
+        m &= m - 1;
+        lists[pos++] = static_cast<uint16_t>((lane << 5) | b);
+      }
+      __syncwarp();
+      for (int e = lane; e < total; e += 32) {
+        const int ent = lists[e];
+        const int tt = c0 + (ent >> 5);
+        const int y = ny_lo + tt / nw, j = tt % nw;
+        const int x = bx0 + kOwn * j + (ent & 31);
+        const uint16_t* row = tile_s + (y - fy0) * P.rp + (x - tx0);
+        const int s = row[0];
+        if (s == 0) continue;  // a corner whose score is 0 (MT, eps 0) is no candidate
+        bool keep = true;
+        if (P.stats) {
+          ++n_cand;
+          uint32_t cmp = 0;
+          for (int rr = 1; rr <= n && keep; ++rr) {
+            auto visit = [&](int dx, int dy) {
+              if (!keep) return;
+              const int nx = x + dx, ny = y + dy;
+              if (nx < 0 || ny < 0 || nx >= w || ny >= h) return;
+              ++cmp;
+              const int v = row[dy * P.rp + dx];
+              if (v > s || (v == s && (dy < 0 || (dy == 0 && dx < 0)))) keep = false;
+            };
+            for (int dx = -rr; dx <= rr; ++dx) visit(dx, -rr);
+            for (int dy = -rr + 1; dy <= rr; ++dy) visit(rr, dy);
+            for (int dx = rr - 1; dx >= -rr; --dx) visit(dx, rr);
+            for (int dy = rr - 1; dy >= -rr + 1; --dy) visit(-rr, dy);
+          }
+          n_cmp += cmp;
+        } else {
+          // out-of-image neighbours read the tile's zero margin: 0 < s never suppresses
+          for (int dy = -n; dy <= n && keep; ++dy)
+            for (int dx = -n; dx <= n; ++dx) {
+              const int v = row[dy * P.rp + dx];
+              const bool earlier = dy < 0 || (dy == 0 && dx < 0);
+              if (v > s || (v == s && earlier)) {
+                keep = false;
+                break;
+              }
+            }
+        }
+        if (!keep) continue;
+        const int X = x << k, Y = y << k;
+        const int ccx = X / P.cell_w, ccy = Y / P.cell_h;
+        if (local_keys) {
+          const int ox = (ccx * P.cell_w + (1 << k) - 1) >> k;
+          const int oy = (ccy * P.cell_h + (1 << k) - 1) >> k;
+          const uint32_t key = (static_cast<uint32_t>(s) << 20) |
+                               (static_cast<uint32_t>(1023 - (y - oy)) << 10) |
+                               static_cast<uint32_t>(1023 - (x - ox));
+          atomicMax(skeys + (ccy - cr0) * P.cols + ccx, key);
+        } else {
+          atomicMax(P.keys + static_cast<size_t>(f) * P.cells + ccy * P.cols + ccx,
+                    pack_key(s, k, X, Y));
+        }
+      }
+      __syncwarp();
+    }
+  }
+  if (P.stats) {
+    for (int o = 16; o; o >>= 1) {
+      n_cand += __shfl_xor_sync(0xffffffffu, n_cand, o);
+      n_cmp += __shfl_xor_sync(0xffffffffu, n_cmp, o);
+    }
+    if (lane == 0 && (n_cand | n_cmp)) {
+      atomicAdd(P.stats + 2 * f, n_cand);
+      atomicAdd(P.stats + 2 * f + 1, n_cmp);
+    }
+  }
+  if (!local_keys) return;
+  __syncthreads();
+
+  // --- 6. flush the shared cell keys into the frame's global keys
+  for (int i = tid; i < slots; i += kThreads) {
+    const uint32_t key = skeys[i];
+    if (!key) continue;
+    const int ccy = cr0 + i / P.cols, ccx = i % P.cols;
+    const int ox = (ccx * P.cell_w + (1 << k) - 1) >> k;
+    const int oy = (ccy * P.cell_h + (1 << k) - 1) >> k;
+    const int y = oy + 1023 - static_cast<int>((key >> 10) & 1023u);
+    const int x = ox + 1023 - static_cast<int>(key & 1023u);
+    atomicMax(P.keys + static_cast<size_t>(f) * P.cells + i + cr0 * P.cols,
+              pack_key(static_cast<int>(key >> 20), k, x << k, y << k));
+  }
+}
+
+}  // namespace fused
+}  // namespace flkb

@@ -112,7 +112,7 @@ class _DevBuf:
 
     def __init__(self, ptr: int, nbytes: int):
         self.__cuda_array_interface__ = {"shape": (nbytes,), "typestr": "|u1",
-                                         "data": (ptr, True), "version": 3}
+                                         "data": (ptr, False), "version": 3}
 
 
 def read_device(ptr: int, nbytes: int) -> np.ndarray:
