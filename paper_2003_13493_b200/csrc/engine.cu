@@ -8,6 +8,7 @@
 
 #include "conformance.cuh"
 #include "engine.hpp"
+#include "fused_dispatch.hpp"
 #include "kernels_fused.cuh"
 #include "kernels_v1.cuh"
 
@@ -153,30 +154,6 @@ int DeviceBatch::kernels_per_run() const { return g_.levels + 1; }
 
 namespace {
 
-using FusedFn = void (*)(const fused::Params);
-
-template <int N>
-FusedFn fused_for_kind(int kind) {
-  switch (kind) {
-    case kSadB: return fused::k_detect<N, kSadB>;
-    case kSadA: return fused::k_detect<N, kSadA>;
-    default: return fused::k_detect<N, kMt>;
-  }
-}
-
-FusedFn fused_kernel(int n, int kind) {
-  switch (n) {
-    case 9: return fused_for_kind<9>(kind);
-    case 10: return fused_for_kind<10>(kind);
-    case 11: return fused_for_kind<11>(kind);
-    case 12: return fused_for_kind<12>(kind);
-    case 13: return fused_for_kind<13>(kind);
-    case 14: return fused_for_kind<14>(kind);
-    case 15: return fused_for_kind<15>(kind);
-    default: return fused_for_kind<16>(kind);
-  }
-}
-
 constexpr int kFusedSmemTarget = 112 * 1024;  // two CTAs per SM
 constexpr int kFusedSmemMax = 227 * 1024;
 
@@ -190,6 +167,8 @@ fused::Params fused_geometry(const DetectParams& p, const Geometry& g, int R, in
   P.R = R;
   P.cell_w = p.cell_w;
   P.cell_h = p.cell_h;
+  P.div_cw = fused::FastDiv::make(static_cast<uint32_t>(p.cell_w));
+  P.div_ch = fused::FastDiv::make(static_cast<uint32_t>(p.cell_h));
   P.cols = g.cols;
   P.cells = g.cells;
   const int n = p.radius;
@@ -198,7 +177,8 @@ fused::Params fused_geometry(const DetectParams& p, const Geometry& g, int R, in
     fused::Level& L = P.lv[k];
     L.w = g.lw[k];
     L.h = g.lh[k];
-    L.tiles_x = std::max(1, std::min(tiles0, (L.w + 63) / 64));
+    // u16 corner-list entries address stage columns below 1024: tiles <= 928 px
+    L.tiles_x = std::max(std::max(1, std::min(tiles0, (L.w + 63) / 64)), (L.w + 927) / 928);
     L.tile_w = (L.w + L.tiles_x - 1) / L.tiles_x;
     L.tiles_x = (L.w + L.tile_w - 1) / L.tile_w;
     L.bands = (L.h + R - 1) / R;
@@ -238,7 +218,7 @@ void DeviceBatch::run(const uint8_t* frames, size_t fstride, int pitch, int coun
     run_staged(frames, fstride, pitch, count, stats, s, times, first);
     return;
   }
-  const FusedFn kern = fused_kernel(p_.arc_length, p_.score);
+  const fused::KernelFn kern = fused::kernel_for(p_.arc_length, p_.score, p_.radius);
   if (static_cast<size_t>(smem) > fused_smem_) {
     check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
                "fused smem attribute");

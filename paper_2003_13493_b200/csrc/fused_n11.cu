@@ -1,0 +1,4 @@
+// Fused detector kernels for arc length N = 11 (see kernels_fused.cuh).
+#include "fused_dispatch.hpp"
+
+FLKB_FUSED_INSTANTIATE(11)

@@ -41,6 +41,23 @@ constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
 constexpr int kMaxLv = 16;
 
+// Exact x / d for 0 <= x < 2^31 with one IMAD.HI: q = (umulhi(x, m) + x) >> l,
+// l = ceil(log2 d), m = 1 + floor(2^32 (2^l - d) / d).
+struct FastDiv {
+  uint32_t m = 1;
+  int l = 0;
+  static FastDiv make(uint32_t d) {
+    FastDiv f;
+    f.l = 0;
+    while ((1ull << f.l) < d) ++f.l;
+    f.m = static_cast<uint32_t>(1ull + ((1ull << 32) * ((1ull << f.l) - d)) / d);
+    return f;
+  }
+  __device__ __forceinline__ int operator()(int x) const {
+    return static_cast<int>((__umulhi(static_cast<uint32_t>(x), m) + static_cast<uint32_t>(x)) >> l);
+  }
+};
+
 struct Level {
   const uint8_t* img;  // frame 0, row 0
   size_t fstride;
@@ -56,6 +73,7 @@ struct Params {
   int levels;
   int eps, radius, R;
   int cell_w, cell_h, cols, cells;
+  FastDiv div_cw, div_ch;
   int sw;         // stage row pitch (bytes)
   int nw_max;     // plane words per row, max over tiles
   int rp;         // score tile pitch (u16)
@@ -205,7 +223,27 @@ __device__ __forceinline__ int sad_b_packed(const uint32_t (&r)[4], uint32_t c, 
 
 // ---------------------------------------------------------------- kernel
 
-template <int N, int KIND>
+// Per-thread walk over a row-major (rows x nw) task grid with stride kThreads,
+// without a division per step.
+struct TaskIter {
+  int row, j, drow, dj, nw;
+  __device__ __forceinline__ TaskIter(int t0, int nw_) : nw(nw_) {
+    row = t0 / nw_;
+    j = t0 - row * nw_;
+    drow = kThreads / nw_;
+    dj = kThreads - drow * nw_;
+  }
+  __device__ __forceinline__ void next() {
+    row += drow;
+    j += dj;
+    if (j >= nw) {
+      j -= nw;
+      ++row;
+    }
+  }
+};
+
+template <int N, int KIND, int RADIUS>
 __global__ void __launch_bounds__(kThreads, 2) k_detect(const __grid_constant__ Params P) {
   extern __shared__ __align__(128) uint8_t smem[];
   const Smem S = smem_layout(P);
@@ -218,7 +256,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_detect(const __grid_constant__ 
   const int local = blockIdx.x - L.cta0;
   const int band = local / L.tiles_x, tile = local % L.tiles_x;
   const int f = blockIdx.y;
-  const int n = P.radius, w = L.w, h = L.h;
+  const int n = RADIUS > 0 ? RADIUS : P.radius, w = L.w, h = L.h;
   const int y0 = band * P.R, y1 = min(y0 + P.R, h);          // rows suppressed here
   const int x_lo = tile * L.tile_w, x_hi = min(x_lo + L.tile_w, w);
   const int fy0 = y0 - n;                                       // tile row 0 <-> image row fy0
@@ -234,12 +272,13 @@ __global__ void __launch_bounds__(kThreads, 2) k_detect(const __grid_constant__ 
   uint16_t* tile_s = reinterpret_cast<uint16_t*>(smem + S.planes);
   uint32_t* cm = reinterpret_cast<uint32_t*>(smem + S.cm);
   uint16_t* lists = reinterpret_cast<uint16_t*>(smem + S.lists) + warp * (32 * kOwn);
+  (void)lane;
   uint32_t* skeys = reinterpret_cast<uint32_t*>(smem + S.skeys);
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + S.bar);
 
   // cell rows touched by the suppressed rows [y0, y1) of level k
-  const int cr0 = (y0 << k) / P.cell_h;
-  const int cr1 = y1 > y0 ? ((y1 - 1) << k) / P.cell_h : cr0;
+  const int cr0 = P.div_ch(y0 << k);
+  const int cr1 = y1 > y0 ? P.div_ch((y1 - 1) << k) : cr0;
   const int slots = (cr1 - cr0 + 1) * P.cols;
   const bool local_keys = slots <= P.key_slots;
 
@@ -293,8 +332,9 @@ __global__ void __launch_bounds__(kThreads, 2) k_detect(const __grid_constant__ 
   // --- 2. bit planes of every staged row
   {
     const int tasks = (yb - ya) * nw;
-    for (int t = tid; t < tasks; t += kThreads) {
-      const int r = ya - iy0 + t / nw, j = t % nw;
+    TaskIter it(tid, nw);
+    for (int t = tid; t < tasks; t += kThreads, it.next()) {
+      const int r = ya - iy0 + it.row, j = it.j;
       const int bx = kOwn * j;
       const uint32_t* src = reinterpret_cast<const uint32_t*>(stage + r * P.sw + (bx & ~3));
       uint32_t a[9], wv[8], pl[8];
@@ -318,8 +358,9 @@ __global__ void __launch_bounds__(kThreads, 2) k_detect(const __grid_constant__ 
 #pragma unroll
     for (int b = 0; b < 8; ++b) E[b] = ((P.eps >> b) & 1) ? 0xFFFFFFFFu : 0u;
     const int tasks = max(fast_rows, 0) * nw;
-    for (int t = tid; t < tasks; t += kThreads) {
-      const int y = cy_lo + t / nw, j = t % nw;
+    TaskIter it(tid, nw);
+    for (int t = tid; t < tasks; t += kThreads, it.next()) {
+      const int y = cy_lo + it.row, j = it.j;
       const int r = y - iy0;  // stage/plane row of the centre
       const uint32_t* base = planes + j * 8;
       auto row_planes = [&](int rr, uint32_t (&q)[8]) {
@@ -368,7 +409,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_detect(const __grid_constant__ 
       const uint32_t valid = hi_b > lo_b ? ((hi_b >= 32 ? 0xFFFFFFFFu : ((1u << hi_b) - 1u)) &
                                             ~((1u << lo_b) - 1u))
                                          : 0u;
-      cm[(y - cy_lo) * nw + j] = corner & valid;
+      cm[t] = corner & valid;
     }
   }
   __syncthreads();
@@ -381,53 +422,67 @@ __global__ void __launch_bounds__(kThreads, 2) k_detect(const __grid_constant__ 
     for (int i = tid; i < n16; i += kThreads) z[i] = make_uint4(0, 0, 0, 0);
   }
   __syncthreads();
-  // tile column of image x: x - (x_lo - n) + n  (left zero margin of n)
-  const int tx0 = x_lo - 2 * n;
-  auto stage_px = [&](int y, int x) -> uint32_t { return stage[(y - iy0) * P.sw + (x - bx0)]; };
+  // Score-tile column of stage column xs: xs + bx0 - (x_lo - 2n), i.e. an n-wide
+  // zero margin left of the FAST columns.
+  const int tcol = bx0 - (x_lo - 2 * n);
+  int rowoff[7];  // stage offsets of ring rows dy = -3..3
+#pragma unroll
+  for (int d = 0; d < 7; ++d) rowoff[d] = (d - 3) * P.sw;
+
+  // Warp-level compaction of one 32-task chunk: every set bit of the lane's
+  // corner word becomes a u16 entry (row within the chunk << 10 | stage
+  // column); returns the entry count.
+  auto compact = [&](uint32_t m, int row_rel, int j) -> int {
+    const int cnt = __popc(m);
+    int incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += v;
+    }
+    int pos = incl - cnt;
+    const uint32_t base = (static_cast<uint32_t>(row_rel) << 10) | static_cast<uint32_t>(kOwn * j);
+    while (m) {
+      const int b = __ffs(m) - 1;
+      m &= m - 1;
+      lists[pos++] = static_cast<uint16_t>(base + b);
+    }
+    const int total = __shfl_sync(0xffffffffu, incl, 31);
+    __syncwarp();
+    return total;
+  };
+
   {
     const int tasks = max(fast_rows, 0) * nw;
-    for (int c0 = warp * 32; c0 < tasks; c0 += kThreads) {
+    TaskIter it(warp * 32 + lane, nw);
+    for (int c0 = warp * 32; c0 < tasks; c0 += kThreads, it.next()) {
       const int t = c0 + lane;
-      uint32_t m = t < tasks ? cm[t] : 0u;
-      const int cnt = __popc(m);
-      int incl = cnt;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int v = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += v;
-      }
-      const int total = __shfl_sync(0xffffffffu, incl, 31);
-      int pos = incl - cnt;
-      while (m) {
-        const int b = __ffs(m) - 1;
-        m &= m - 1;
-        lists[pos++] = static_cast<uint16_t>((lane << 5) | b);
-      }
-      __syncwarp();
+      const int row_c = __shfl_sync(0xffffffffu, it.row, 0);  // chunk's first row
+      const uint32_t m = t < tasks ? cm[t] : 0u;
+      const int total = compact(m, it.row - row_c, it.j);
       for (int e = lane; e < total; e += 32) {
         const int ent = lists[e];
-        const int tt = c0 + (ent >> 5);
-        const int y = cy_lo + tt / nw, j = tt % nw;
-        const int x = bx0 + kOwn * j + (ent & 31);
-        const uint32_t cc = stage_px(y, x);
-        int s;
+        const int y = cy_lo + row_c + (ent >> 10), xs = ent & 1023;
+        const uint8_t* sp = stage + (y - iy0) * P.sw + xs;
+        const uint32_t cc = sp[0];
+        int sc;
         if (KIND == kSadB) {
           uint32_t rb[16];
 #pragma unroll
-          for (int i = 0; i < 16; ++i) rb[i] = stage_px(y + ring_dy(i), x + ring_dx(i));
+          for (int i = 0; i < 16; ++i) rb[i] = sp[rowoff[ring_dy(i) + 3] + ring_dx(i)];
           uint32_t pk[4];
 #pragma unroll
           for (int q = 0; q < 4; ++q)
             pk[q] = __byte_perm(__byte_perm(rb[4 * q], rb[4 * q + 1], 0x0040),
                                 __byte_perm(rb[4 * q + 2], rb[4 * q + 3], 0x0040), 0x5410);
-          s = sad_b_packed(pk, cc, static_cast<uint32_t>(P.eps));
+          sc = sad_b_packed(pk, cc, static_cast<uint32_t>(P.eps));
         } else {
           int ring[16];
 #pragma unroll
-          for (int i = 0; i < 16; ++i) ring[i] = stage_px(y + ring_dy(i), x + ring_dx(i));
-          s = fast_score<N, KIND>(static_cast<int>(cc), ring, P.eps);
+          for (int i = 0; i < 16; ++i) ring[i] = sp[rowoff[ring_dy(i) + 3] + ring_dx(i)];
+          sc = fast_score<N, KIND>(static_cast<int>(cc), ring, P.eps);
         }
-        tile_s[(y - fy0) * P.rp + (x - tx0)] = static_cast<uint16_t>(s);
+        tile_s[(y - fy0) * P.rp + xs + tcol] = static_cast<uint16_t>(sc);
       }
       __syncwarp();
     }
@@ -439,41 +494,28 @@ __global__ void __launch_bounds__(kThreads, 2) k_detect(const __grid_constant__ 
   {
     const int ny_lo = max(y0, 3), ny_hi = min(y1, h - 3);
     const int nx_lo = max(x_lo, 3), nx_hi = min(x_hi, w - 3);
-    const int row_off = ny_lo - cy_lo;
+    const int cm0 = (ny_lo - cy_lo) * nw;
     const int tasks = max(ny_hi - ny_lo, 0) * nw;
-    for (int c0 = warp * 32; c0 < tasks; c0 += kThreads) {
+    const int rp = P.rp;
+    TaskIter it(warp * 32 + lane, nw);
+    for (int c0 = warp * 32; c0 < tasks; c0 += kThreads, it.next()) {
       const int t = c0 + lane;
+      const int row_c = __shfl_sync(0xffffffffu, it.row, 0);
       uint32_t m = 0;
       if (t < tasks) {
-        const int j = t % nw;
-        const int xb = bx0 + kOwn * j;
+        const int xb = bx0 + kOwn * it.j;
         const int lo_b = max(3, nx_lo - xb), hi_b = min(29, nx_hi - xb);
         const uint32_t own = hi_b > lo_b ? ((hi_b >= 32 ? 0xFFFFFFFFu : ((1u << hi_b) - 1u)) &
                                             ~((1u << lo_b) - 1u))
                                          : 0u;
-        m = cm[(row_off + t / nw) * nw + j] & own;
+        m = cm[cm0 + t] & own;
       }
-      const int cnt = __popc(m);
-      int incl = cnt;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int v = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += v;
-      }
-      const int total = __shfl_sync(0xffffffffu, incl, 31);
-      int pos = incl - cnt;
-      while (m) {
-        const int b = __ffs(m) - 1;
-        m &= m - 1;
-        lists[pos++] = static_cast<uint16_t>((lane << 5) | b);
-      }
-      __syncwarp();
+      const int total = compact(m, it.row - row_c, it.j);
       for (int e = lane; e < total; e += 32) {
         const int ent = lists[e];
-        const int tt = c0 + (ent >> 5);
-        const int y = ny_lo + tt / nw, j = tt % nw;
-        const int x = bx0 + kOwn * j + (ent & 31);
-        const uint16_t* row = tile_s + (y - fy0) * P.rp + (x - tx0);
+        const int y = ny_lo + row_c + (ent >> 10), xs = ent & 1023;
+        const int x = bx0 + xs;
+        const uint16_t* row = tile_s + (y - fy0) * rp + xs + tcol;
         const int s = row[0];
         if (s == 0) continue;  // a corner whose score is 0 (MT, eps 0) is no candidate
         bool keep = true;
@@ -486,7 +528,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_detect(const __grid_constant__ 
               const int nx = x + dx, ny = y + dy;
               if (nx < 0 || ny < 0 || nx >= w || ny >= h) return;
               ++cmp;
-              const int v = row[dy * P.rp + dx];
+              const int v = row[dy * rp + dx];
               if (v > s || (v == s && (dy < 0 || (dy == 0 && dx < 0)))) keep = false;
             };
             for (int dx = -rr; dx <= rr; ++dx) visit(dx, -rr);
@@ -495,11 +537,16 @@ __global__ void __launch_bounds__(kThreads, 2) k_detect(const __grid_constant__ 
             for (int dy = rr - 1; dy >= -rr + 1; --dy) visit(-rr, dy);
           }
           n_cmp += cmp;
+        } else if (RADIUS == 1) {
+          // earlier neighbours must be strictly lower, later ones not higher;
+          // out-of-image neighbours read the tile's zero margin
+          const int e0 = max(max(row[-rp - 1], row[-rp]), max(row[-rp + 1], row[-1]));
+          const int l0 = max(max(row[1], row[rp - 1]), max(row[rp], row[rp + 1]));
+          keep = e0 < s && l0 <= s;
         } else {
-          // out-of-image neighbours read the tile's zero margin: 0 < s never suppresses
           for (int dy = -n; dy <= n && keep; ++dy)
             for (int dx = -n; dx <= n; ++dx) {
-              const int v = row[dy * P.rp + dx];
+              const int v = row[dy * rp + dx];
               const bool earlier = dy < 0 || (dy == 0 && dx < 0);
               if (v > s || (v == s && earlier)) {
                 keep = false;
@@ -509,7 +556,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_detect(const __grid_constant__ 
         }
         if (!keep) continue;
         const int X = x << k, Y = y << k;
-        const int ccx = X / P.cell_w, ccy = Y / P.cell_h;
+        const int ccx = P.div_cw(X), ccy = P.div_ch(Y);
         if (local_keys) {
           const int ox = (ccx * P.cell_w + (1 << k) - 1) >> k;
           const int oy = (ccy * P.cell_h + (1 << k) - 1) >> k;
