@@ -2,6 +2,7 @@
 // buffers, launch plan, stage timing, conformance and synthetic frames.
 #include <atomic>
 #include <cstddef>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -154,7 +155,8 @@ int DeviceBatch::kernels_per_run() const { return g_.levels + 1; }
 
 namespace {
 
-constexpr int kFusedSmemTarget = 112 * 1024;  // two CTAs per SM
+// kMinBlocks CTAs per SM (1 KB of each CTA's share is reserved by the driver)
+constexpr int kFusedSmemTarget = (228 * 1024) / fused::kMinBlocks - 1024;
 constexpr int kFusedSmemMax = 227 * 1024;
 
 // Shared-memory geometry of the fused kernel for column tiles of at most
@@ -206,9 +208,16 @@ void DeviceBatch::run(const uint8_t* frames, size_t fstride, int pitch, int coun
   if (pitch < g_.width) throw InvalidArgument("row pitch smaller than the frame width");
   if (count > 65535) throw InvalidArgument("at most 65535 frames per launch");
   DeviceGuard guard(device_);
-  const int R = fused_R_;
+  int R = fused_R_;
+  const char* forced = std::getenv("FLKB_BAND_ROWS");  // tuning override
+  if (forced) R = std::max(4, std::atoi(forced));
   int tiles0 = 1;
   fused::Params P = fused_geometry(p_, g_, R, tiles0);
+  // shrink the band until kMinBlocks CTAs fit one SM, then split columns
+  while (!forced && fused::smem_layout(P).total > kFusedSmemTarget && R > 16) {
+    R -= 4;
+    P = fused_geometry(p_, g_, R, tiles0);
+  }
   while (fused::smem_layout(P).total > kFusedSmemTarget && P.lv[0].tile_w > 64) {
     ++tiles0;
     P = fused_geometry(p_, g_, R, tiles0);

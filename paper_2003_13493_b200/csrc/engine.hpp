@@ -115,7 +115,7 @@ class DeviceBatch {
   uint64_t* d_stats_ = nullptr;  // [capacity][2] = candidates, comparisons
   float* d_naive_ = nullptr;     // conformance scratch (lazily allocated)
   size_t fused_smem_ = 0;        // dynamic shared memory of the fused kernel
-  int fused_R_ = 32;             // rows per band
+  int fused_R_ = 32;             // rows per band (largest that fits kMinBlocks CTAs/SM)
   int fused_tile_w_[kMaxLevels] = {};
   int* d_conf_ = nullptr;
 };

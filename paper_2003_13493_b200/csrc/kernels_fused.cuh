@@ -39,6 +39,10 @@ namespace fused {
 constexpr int kOwn = 26;       // pixels owned by one 32-bit plane word
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
+#ifndef FLKB_MIN_BLOCKS
+#define FLKB_MIN_BLOCKS 3
+#endif
+constexpr int kMinBlocks = FLKB_MIN_BLOCKS;  // CTAs per SM the register budget targets
 constexpr int kMaxLv = 16;
 
 // Exact x / d for 0 <= x < 2^31 with one IMAD.HI: q = (umulhi(x, m) + x) >> l,
@@ -244,7 +248,7 @@ struct TaskIter {
 };
 
 template <int N, int KIND, int RADIUS>
-__global__ void __launch_bounds__(kThreads, 2) k_detect(const __grid_constant__ Params P) {
+__global__ void __launch_bounds__(kThreads, kMinBlocks) k_detect(const __grid_constant__ Params P) {
   extern __shared__ __align__(128) uint8_t smem[];
   const Smem S = smem_layout(P);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
