@@ -87,8 +87,15 @@ struct Params {
 };
 
 struct Smem {
-  int stage, planes, cm, lists, skeys, bar, total;
+  int stage, planes, cm, list, scan, skeys, bar, total;
 };
+
+// Corner-list capacity (u16 entries); a band with more corners is scored in
+// several rounds.
+__host__ __device__ inline int list_capacity(const Params& p) {
+  const int worst = (p.R + 2 * p.radius) * p.nw_max * kOwn;
+  return worst < 6144 ? (worst + 7) & ~7 : 6144;
+}
 
 __host__ __device__ inline Smem smem_layout(const Params& p) {
   const int img_rows = p.R + 2 * p.radius + 6;
@@ -98,7 +105,7 @@ __host__ __device__ inline Smem smem_layout(const Params& p) {
   s.stage = off;
   off += img_rows * p.sw;
   off = (off + 127) & ~127;
-  s.planes = off;  // aliased by the score tile after the mask phase
+  s.planes = off;  // [2 halves][img_rows][nw_max][4 planes]; the score tile aliases it later
   const int pl = img_rows * p.nw_max * 32;
   const int rt = fast_rows * p.rp * 2;
   off += pl > rt ? pl : rt;
@@ -106,8 +113,11 @@ __host__ __device__ inline Smem smem_layout(const Params& p) {
   s.cm = off;
   off += fast_rows * p.nw_max * 4;
   off = (off + 15) & ~15;
-  s.lists = off;
-  off += kWarps * 32 * kOwn * 2;
+  s.list = off;
+  off += list_capacity(p) * 2;
+  off = (off + 15) & ~15;
+  s.scan = off;
+  off += (kWarps + 4) * 4;
   off = (off + 15) & ~15;
   s.skeys = off;
   off += p.key_slots * 4;
@@ -275,8 +285,11 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_detect(const __grid_co
   uint32_t* planes = reinterpret_cast<uint32_t*>(smem + S.planes);
   uint16_t* tile_s = reinterpret_cast<uint16_t*>(smem + S.planes);
   uint32_t* cm = reinterpret_cast<uint32_t*>(smem + S.cm);
-  uint16_t* lists = reinterpret_cast<uint16_t*>(smem + S.lists) + warp * (32 * kOwn);
-  (void)lane;
+  uint16_t* list = reinterpret_cast<uint16_t*>(smem + S.list);
+  int* scan = reinterpret_cast<int*>(smem + S.scan);
+  // planes: low half (bit planes 0-3) and high half (4-7) in separate arrays
+  // so a warp's 16-byte accesses to consecutive words are bank-conflict free
+  const int half = (P.R + 2 * n + 6) * P.nw_max * 4;
   uint32_t* skeys = reinterpret_cast<uint32_t*>(smem + S.skeys);
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + S.bar);
 
@@ -348,9 +361,9 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_detect(const __grid_co
 #pragma unroll
       for (int i = 0; i < 8; ++i) wv[i] = __byte_perm(a[i], a[i + 1], sel);
       transpose32x8(wv, pl);
-      uint4* dst = reinterpret_cast<uint4*>(planes + (r * P.nw_max + j) * 8);
-      dst[0] = make_uint4(pl[0], pl[1], pl[2], pl[3]);
-      dst[1] = make_uint4(pl[4], pl[5], pl[6], pl[7]);
+      uint32_t* dst = planes + (r * P.nw_max + j) * 4;
+      *reinterpret_cast<uint4*>(dst) = make_uint4(pl[0], pl[1], pl[2], pl[3]);
+      *reinterpret_cast<uint4*>(dst + half) = make_uint4(pl[4], pl[5], pl[6], pl[7]);
     }
   }
   __syncthreads();
@@ -366,10 +379,11 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_detect(const __grid_co
     for (int t = tid; t < tasks; t += kThreads, it.next()) {
       const int y = cy_lo + it.row, j = it.j;
       const int r = y - iy0;  // stage/plane row of the centre
-      const uint32_t* base = planes + j * 8;
+      const uint32_t* base = planes + j * 4;
       auto row_planes = [&](int rr, uint32_t (&q)[8]) {
-        const uint4* s4 = reinterpret_cast<const uint4*>(base + rr * P.nw_max * 8);
-        const uint4 u = s4[0], v = s4[1];
+        const uint32_t* q4 = base + rr * P.nw_max * 4;
+        const uint4 u = *reinterpret_cast<const uint4*>(q4);
+        const uint4 v = *reinterpret_cast<const uint4*>(q4 + half);
         q[0] = u.x; q[1] = u.y; q[2] = u.z; q[3] = u.w;
         q[4] = v.x; q[5] = v.y; q[6] = v.z; q[7] = v.w;
       };
@@ -418,107 +432,134 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_detect(const __grid_co
   }
   __syncthreads();
 
-  // --- 4. zero the score tile (aliases the planes), then score corners
-  const int tile_rows = P.R + 2 * n;
+  // --- 4. one CTA-wide corner list (row-major task order) from a block scan
+  //        of per-task corner counts; the score tile (aliasing the dead
+  //        planes) is zeroed meanwhile. Entries: (row - cy_lo) << 10 | stage column.
+  const int tasks_f = max(fast_rows, 0) * nw;
+  const int per = (tasks_f + kThreads - 1) / kThreads;
+  const int tb = min(tid * per, tasks_f), te = min(tb + per, tasks_f);
+  int cnt = 0;
+  for (int t = tb; t < te; ++t) cnt += __popc(cm[t]);
   {
     uint4* z = reinterpret_cast<uint4*>(tile_s);
-    const int n16 = (tile_rows * P.rp * 2) / 16;
+    const int n16 = ((P.R + 2 * n) * P.rp * 2) / 16;
     for (int i = tid; i < n16; i += kThreads) z[i] = make_uint4(0, 0, 0, 0);
   }
+  int incl = cnt;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int v = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += v;
+  }
+  if (lane == 31) scan[warp] = incl;
   __syncthreads();
+  if (warp == 0) {
+    const int v = lane < kWarps ? scan[lane] : 0;
+    int acc = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int u = __shfl_up_sync(0xffffffffu, acc, o);
+      if (lane >= o) acc += u;
+    }
+    if (lane < kWarps) scan[lane] = acc - v;
+    if (lane == 31) scan[kWarps] = acc;
+  }
+  __syncthreads();
+  const int base = scan[warp] + incl - cnt;  // this thread's first list index
+  const int total = scan[kWarps];
+  const int cap = list_capacity(P);
+  const int row_tb = tb / nw, j_tb = tb - row_tb * nw;
+  // Writes the entries with list index in [w0, w0 + cap) to list[index - w0].
+  auto build = [&](int w0) {
+    if (base >= w0 + cap || base + cnt <= w0) return;
+    int pos = base, row = row_tb, j = j_tb;
+    for (int t = tb; t < te; ++t) {
+      uint32_t m = cm[t];
+      const uint32_t e0 = (static_cast<uint32_t>(row) << 10) | static_cast<uint32_t>(kOwn * j);
+      while (m) {
+        const int b = __ffs(m) - 1;
+        m &= m - 1;
+        if (pos >= w0 && pos < w0 + cap) list[pos - w0] = static_cast<uint16_t>(e0 + b);
+        ++pos;
+      }
+      if (++j == nw) {
+        j = 0;
+        ++row;
+      }
+    }
+  };
   // Score-tile column of stage column xs: xs + bx0 - (x_lo - 2n), i.e. an n-wide
   // zero margin left of the FAST columns.
   const int tcol = bx0 - (x_lo - 2 * n);
-  int rowoff[7];  // stage offsets of ring rows dy = -3..3
+  for (int w0 = 0; w0 < total; w0 += cap) {
+    if (w0 > 0) __syncthreads();  // the previous round's entries are consumed
+    build(w0);
+    __syncthreads();
+    const int m_end = min(cap, total - w0);
+    for (int e = tid; e < m_end; e += kThreads) {
+      const int ent = list[e];
+      const int y = cy_lo + (ent >> 10), xs = ent & 1023;
+      const uint8_t* sp = stage + (y - iy0) * P.sw + xs;
+      const uint32_t cc = sp[0];
+      int sc;
+      if (KIND == kSadB) {
+        uint32_t rb[16];
 #pragma unroll
-  for (int d = 0; d < 7; ++d) rowoff[d] = (d - 3) * P.sw;
-
-  // Warp-level compaction of one 32-task chunk: every set bit of the lane's
-  // corner word becomes a u16 entry (row within the chunk << 10 | stage
-  // column); returns the entry count.
-  auto compact = [&](uint32_t m, int row_rel, int j) -> int {
-    const int cnt = __popc(m);
-    int incl = cnt;
+        for (int i = 0; i < 16; ++i) rb[i] = sp[ring_dy(i) * P.sw + ring_dx(i)];
+        uint32_t pk[4];
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int v = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += v;
-    }
-    int pos = incl - cnt;
-    const uint32_t base = (static_cast<uint32_t>(row_rel) << 10) | static_cast<uint32_t>(kOwn * j);
-    while (m) {
-      const int b = __ffs(m) - 1;
-      m &= m - 1;
-      lists[pos++] = static_cast<uint16_t>(base + b);
-    }
-    const int total = __shfl_sync(0xffffffffu, incl, 31);
-    __syncwarp();
-    return total;
-  };
-
-  {
-    const int tasks = max(fast_rows, 0) * nw;
-    TaskIter it(warp * 32 + lane, nw);
-    for (int c0 = warp * 32; c0 < tasks; c0 += kThreads, it.next()) {
-      const int t = c0 + lane;
-      const int row_c = __shfl_sync(0xffffffffu, it.row, 0);  // chunk's first row
-      const uint32_t m = t < tasks ? cm[t] : 0u;
-      const int total = compact(m, it.row - row_c, it.j);
-      for (int e = lane; e < total; e += 32) {
-        const int ent = lists[e];
-        const int y = cy_lo + row_c + (ent >> 10), xs = ent & 1023;
-        const uint8_t* sp = stage + (y - iy0) * P.sw + xs;
-        const uint32_t cc = sp[0];
-        int sc;
-        if (KIND == kSadB) {
-          uint32_t rb[16];
+        for (int q = 0; q < 4; ++q)
+          pk[q] = __byte_perm(__byte_perm(rb[4 * q], rb[4 * q + 1], 0x0040),
+                              __byte_perm(rb[4 * q + 2], rb[4 * q + 3], 0x0040), 0x5410);
+        sc = sad_b_packed(pk, cc, static_cast<uint32_t>(P.eps));
+      } else {
+        int ring[16];
 #pragma unroll
-          for (int i = 0; i < 16; ++i) rb[i] = sp[rowoff[ring_dy(i) + 3] + ring_dx(i)];
-          uint32_t pk[4];
-#pragma unroll
-          for (int q = 0; q < 4; ++q)
-            pk[q] = __byte_perm(__byte_perm(rb[4 * q], rb[4 * q + 1], 0x0040),
-                                __byte_perm(rb[4 * q + 2], rb[4 * q + 3], 0x0040), 0x5410);
-          sc = sad_b_packed(pk, cc, static_cast<uint32_t>(P.eps));
-        } else {
-          int ring[16];
-#pragma unroll
-          for (int i = 0; i < 16; ++i) ring[i] = sp[rowoff[ring_dy(i) + 3] + ring_dx(i)];
-          sc = fast_score<N, KIND>(static_cast<int>(cc), ring, P.eps);
-        }
-        tile_s[(y - fy0) * P.rp + xs + tcol] = static_cast<uint16_t>(sc);
+        for (int i = 0; i < 16; ++i) ring[i] = sp[ring_dy(i) * P.sw + ring_dx(i)];
+        sc = fast_score<N, KIND>(static_cast<int>(cc), ring, P.eps);
       }
-      __syncwarp();
+      tile_s[(y - fy0) * P.rp + xs + tcol] = static_cast<uint16_t>(sc);
     }
   }
   __syncthreads();
 
-  // --- 5. suppression + per-cell keys for candidates in rows [y0, y1)
+  // --- 5. suppression + per-cell keys for the candidates in rows [y0, y1):
+  //        a contiguous range of the list, since tasks are row-major
   unsigned long long n_cand = 0, n_cmp = 0;
   {
     const int ny_lo = max(y0, 3), ny_hi = min(y1, h - 3);
     const int nx_lo = max(x_lo, 3), nx_hi = min(x_hi, w - 3);
-    const int cm0 = (ny_lo - cy_lo) * nw;
-    const int tasks = max(ny_hi - ny_lo, 0) * nw;
-    const int rp = P.rp;
-    TaskIter it(warp * 32 + lane, nw);
-    for (int c0 = warp * 32; c0 < tasks; c0 += kThreads, it.next()) {
-      const int t = c0 + lane;
-      const int row_c = __shfl_sync(0xffffffffu, it.row, 0);
-      uint32_t m = 0;
-      if (t < tasks) {
-        const int xb = bx0 + kOwn * it.j;
-        const int lo_b = max(3, nx_lo - xb), hi_b = min(29, nx_hi - xb);
-        const uint32_t own = hi_b > lo_b ? ((hi_b >= 32 ? 0xFFFFFFFFu : ((1u << hi_b) - 1u)) &
-                                            ~((1u << lo_b) - 1u))
-                                         : 0u;
-        m = cm[cm0 + t] & own;
+    const int T0 = min(max(ny_lo - cy_lo, 0) * nw, tasks_f);
+    const int T1 = min(max(ny_hi - cy_lo, 0) * nw, tasks_f);
+    // list index of task T: the owning thread's base + corners before T
+    if (tid == 0) scan[kWarps + 1] = scan[kWarps + 2] = total;
+    __syncthreads();
+    if (tb < te) {
+      int pos = base;
+      for (int t = tb; t < te; ++t) {
+        if (t == T0) scan[kWarps + 1] = pos;
+        if (t == T1) scan[kWarps + 2] = pos;
+        pos += __popc(cm[t]);
       }
-      const int total = compact(m, it.row - row_c, it.j);
-      for (int e = lane; e < total; e += 32) {
-        const int ent = lists[e];
-        const int y = ny_lo + row_c + (ent >> 10), xs = ent & 1023;
+    }
+    __syncthreads();
+    const int e_lo = T1 > T0 ? scan[kWarps + 1] : 0;
+    const int e_hi = T1 > T0 ? scan[kWarps + 2] : 0;
+    const int rp = P.rp;
+    for (int w0 = e_lo; w0 < e_hi; w0 += cap) {
+      const bool resident = total <= cap;  // the scoring list is still in place
+      const int off = resident ? 0 : w0;
+      if (!resident) {
+        __syncthreads();
+        build(w0);
+        __syncthreads();
+      }
+      const int m_end = resident ? e_hi : min(w0 + cap, e_hi);
+      for (int e = w0 + tid; e < m_end; e += kThreads) {
+        const int ent = list[e - off];
+        const int y = cy_lo + (ent >> 10), xs = ent & 1023;
         const int x = bx0 + xs;
+        if (x < nx_lo || x >= nx_hi) continue;  // halo column of a neighbouring tile
         const uint16_t* row = tile_s + (y - fy0) * rp + xs + tcol;
         const int s = row[0];
         if (s == 0) continue;  // a corner whose score is 0 (MT, eps 0) is no candidate
@@ -573,7 +614,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_detect(const __grid_co
                     pack_key(s, k, X, Y));
         }
       }
-      __syncwarp();
+      if (resident) break;
     }
   }
   if (P.stats) {
