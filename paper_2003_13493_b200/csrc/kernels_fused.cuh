@@ -287,6 +287,8 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_detect(const __grid_co
   uint32_t* cm = reinterpret_cast<uint32_t*>(smem + S.cm);
   uint16_t* list = reinterpret_cast<uint16_t*>(smem + S.list);
   int* scan = reinterpret_cast<int*>(smem + S.scan);
+  uint32_t* colkey = reinterpret_cast<uint32_t*>(stage);  // live once scoring is done
+  uint32_t* rowkey = colkey + P.sw;
   // planes: low half (bit planes 0-3) and high half (4-7) in separate arrays
   // so a warp's 16-byte accesses to consecutive words are bank-conflict free
   const int half = (P.R + 2 * n + 6) * P.nw_max * 4;
@@ -471,6 +473,46 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_detect(const __grid_co
   const int row_tb = tb / nw, j_tb = tb - row_tb * nw;
   // Writes the entries with list index in [w0, w0 + cap) to list[index - w0].
   auto build = [&](int w0) {
+    if (total <= cap) {
+      // Common case, every entry fits: per word slot, the warp either lets each
+      // lane walk its own bits (cost ~ max popc) or expands the non-empty words
+      // one at a time across the lanes (cost ~ non-empty words), whichever is
+      // cheaper for this slot.
+      int pos = base, row = row_tb, j = j_tb;
+      for (int q = 0; q < per; ++q) {
+        const int t = tb + q;
+        uint32_t m = t < te ? cm[t] : 0u;
+        const uint32_t e0 = (static_cast<uint32_t>(row) << 10) | static_cast<uint32_t>(kOwn * j);
+        const int c = __popc(m);
+        const unsigned nz = __ballot_sync(0xffffffffu, m != 0u);
+        const int mx = __reduce_max_sync(0xffffffffu, c);
+        if (2 * mx <= 3 * __popc(nz)) {
+          int p = pos;
+          while (m) {
+            const int b = __ffs(m) - 1;
+            m &= m - 1;
+            list[p++] = static_cast<uint16_t>(e0 + b);
+          }
+        } else {
+          unsigned z = nz;
+          while (z) {
+            const int src = __ffs(z) - 1;
+            z &= z - 1;
+            const uint32_t wv = __shfl_sync(0xffffffffu, m, src);
+            const int p = __shfl_sync(0xffffffffu, pos, src);
+            const uint32_t e = __shfl_sync(0xffffffffu, e0, src);
+            if ((wv >> lane) & 1u)
+              list[p + __popc(wv & ((1u << lane) - 1u))] = static_cast<uint16_t>(e + lane);
+          }
+        }
+        pos += c;
+        if (++j == nw) {
+          j = 0;
+          ++row;
+        }
+      }
+      return;
+    }
     if (base >= w0 + cap || base + cnt <= w0) return;
     int pos = base, row = row_tb, j = j_tb;
     for (int t = tb; t < te; ++t) {
@@ -542,6 +584,24 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_detect(const __grid_co
         pos += __popc(cm[t]);
       }
     }
+    // In-cell key parts per stage column and per tile row, in the dead stage:
+    // colkey = cell_x << 10 | (1023 - local x), rowkey = slot row base << 10 |
+    // (1023 - local y). A survivor's key and slot are then two loads away.
+    if (local_keys) {
+      for (int xs = tid; xs < P.sw; xs += kThreads) {
+        const int x = max(bx0 + xs, 0);
+        const int ccx = P.div_cw(x << k);
+        const int ox = (ccx * P.cell_w + (1 << k) - 1) >> k;
+        colkey[xs] = (static_cast<uint32_t>(ccx) << 10) | ((1023u - (x - ox)) & 1023u);
+      }
+      for (int r = tid; r < fast_rows; r += kThreads) {
+        const int y = cy_lo + r;
+        const int ccy = P.div_ch(y << k);
+        const int oy = (ccy * P.cell_h + (1 << k) - 1) >> k;
+        rowkey[r] = (static_cast<uint32_t>(max(ccy - cr0, 0) * P.cols) << 10) |
+                    ((1023u - (y - oy)) & 1023u);
+      }
+    }
     __syncthreads();
     const int e_lo = T1 > T0 ? scan[kWarps + 1] : 0;
     const int e_hi = T1 > T0 ? scan[kWarps + 2] : 0;
@@ -600,17 +660,13 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_detect(const __grid_co
             }
         }
         if (!keep) continue;
-        const int X = x << k, Y = y << k;
-        const int ccx = P.div_cw(X), ccy = P.div_ch(Y);
         if (local_keys) {
-          const int ox = (ccx * P.cell_w + (1 << k) - 1) >> k;
-          const int oy = (ccy * P.cell_h + (1 << k) - 1) >> k;
-          const uint32_t key = (static_cast<uint32_t>(s) << 20) |
-                               (static_cast<uint32_t>(1023 - (y - oy)) << 10) |
-                               static_cast<uint32_t>(1023 - (x - ox));
-          atomicMax(skeys + (ccy - cr0) * P.cols + ccx, key);
+          const uint32_t ck = colkey[xs], rk = rowkey[y - cy_lo];
+          const uint32_t key = (static_cast<uint32_t>(s) << 20) | ((rk & 1023u) << 10) | (ck & 1023u);
+          atomicMax(skeys + (rk >> 10) + (ck >> 10), key);
         } else {
-          atomicMax(P.keys + static_cast<size_t>(f) * P.cells + ccy * P.cols + ccx,
+          const int X = x << k, Y = y << k;
+          atomicMax(P.keys + static_cast<size_t>(f) * P.cells + P.div_ch(Y) * P.cols + P.div_cw(X),
                     pack_key(s, k, X, Y));
         }
       }
