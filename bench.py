@@ -62,6 +62,20 @@ def hbm_peak():
     return 6650.0, "fallback 6.65 TB/s (B200_PROFILING.md)"
 
 
+def profiled_traffic(frames: int):
+    """DRAM bytes of the fused kernel from the committed ncu capture
+    (profiles/traffic.json: per-frame dram__bytes_read + dram__bytes_write),
+    scaled to this launch's frame count."""
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    if not os.path.exists(p):
+        return None, None
+    try:
+        d = json.load(open(p))
+        return d["dram_bytes_per_frame"] * frames, d["source"]
+    except Exception:
+        return None, None
+
+
 class ClockSampler:
     """nvidia-smi sampling of SM clocks and throttle reasons during the timed region."""
 
@@ -256,11 +270,25 @@ def main():
     h2d = B * W * H
     d2h = 4 * B + 24 * batch.frame_capacity * B
 
+    # dominant-kernel time for the roofline: CUDA events around each launch of
+    # one step, on the launching stream, averaged over a few synchronized steps
+    reps = 5
+    acc = [0.0, 0.0, 0.0]
+    for _ in range(reps):
+        t3 = batch.run_device_timed(frames.data_ptr(), PITCH * H, PITCH, B, stream)
+        acc = [a + b for a, b in zip(acc, t3)]
+    pyr_us, fused_us, comp_us = (a / reps for a in acc)
+    stage_times = (fused_us, pyr_us, comp_us)
+
     if rank == 0:
         peak, peak_src = hbm_peak()
         feats_mean = float(counts.mean())
+        # every pyramid pixel crosses HBM once + 16 B per feature
         bytes_frame = level_pixels() + 16 * feats_mean
-        achieved = bytes_frame * B / (ms_step / 1e3) / 1e9
+        step_achieved = bytes_frame * B / (ms_step / 1e3) / 1e9
+        fused_us, pyr_us, comp_us = stage_times
+        achieved = bytes_frame * B / (fused_us / 1e6) / 1e9
+        traffic, traffic_src = profiled_traffic(B)
         line = {
             "metric": METRIC, "value": fps, "unit": "frames/s", "n_gpus": world,
             "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": ms_step,
@@ -276,10 +304,15 @@ def main():
                     "d2h_bytes_per_step": d2h,
                     "api": "flkb_batch_run_host + flkb_batch_download, pinned host buffers"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": None,
-                         "kernel": f"detection kernels of one step ({batch.kernels_per_run} "
-                                   f"launches per {B}-frame batch)",
-                         "bytes_per_frame": bytes_frame, "peak_source": peak_src},
+                         "frac": achieved / peak, "traffic": traffic,
+                         "kernel": "flkb::fused::k_detect (FAST + score + NMS + cell keys, all "
+                                   f"levels, one launch per {B}-frame batch)",
+                         "kernel_us_per_launch": fused_us,
+                         "kernel_share_of_step": fused_us / (fused_us + pyr_us + comp_us),
+                         "other_kernels_us": {"pyramid": pyr_us, "compact": comp_us},
+                         "bytes_per_frame": bytes_frame, "bytes_per_launch": bytes_frame * B,
+                         "step_achieved_gbs": step_achieved, "peak_source": peak_src,
+                         "traffic_source": traffic_src},
             "gpu_launches": int(launches),
             "clocks": clocks.summary(),
         }

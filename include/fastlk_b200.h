@@ -56,6 +56,13 @@ FLK_API flk_status flkb_batch_run_device(flkb_batch* batch, const uint8_t* frame
                                          size_t frame_stride, int row_pitch, int count,
                                          int with_stats, void* stream);
 
+/* flkb_batch_run_device, synchronized, with CUDA-event device times of its
+ * three launches in stage_us: [0] pyramid, [1] fused FAST + suppression +
+ * cell selection, [2] feature compaction (microseconds). */
+FLK_API flk_status flkb_batch_run_device_timed(flkb_batch* batch, const uint8_t* frames,
+                                               size_t frame_stride, int row_pitch, int count,
+                                               void* stream, double* stage_us);
+
 /* Same, from host memory: H2D copies of the frames happen inside the call on
  * `stream` (pinned host memory overlaps; pageable is staged). */
 FLK_API flk_status flkb_batch_run_host(flkb_batch* batch, const uint8_t* frames,

@@ -565,6 +565,21 @@ flk_status flkb_batch_run_device(flkb_batch* b, const uint8_t* frames, size_t fr
   });
 }
 
+flk_status flkb_batch_run_device_timed(flkb_batch* b, const uint8_t* frames, size_t frame_stride,
+                                       int row_pitch, int count, void* stream, double* stage_us) {
+  if (!b || !frames || !stage_us)
+    return fail(FLK_E_INVALID_ARG, "batch, frames, and stage_us must not be NULL");
+  return guarded([&] {
+    flkb::StageTimes t;
+    b->batch->run(frames, frame_stride, row_pitch, count, false,
+                  static_cast<cudaStream_t>(stream), &t);
+    stage_us[0] = t.pyramid_us;
+    stage_us[1] = t.crf_us;
+    stage_us[2] = t.nms_us;
+    return FLK_OK;
+  });
+}
+
 flk_status flkb_batch_run_host(flkb_batch* b, const uint8_t* frames, size_t frame_stride,
                                int row_pitch, int count, void* stream) {
   if (!b || !frames) return fail(FLK_E_INVALID_ARG, "batch and frames must not be NULL");

@@ -102,7 +102,7 @@ EXT_SYMBOLS = [
     "flkb_batch_run_host", "flkb_batch_download", "flkb_batch_frame_capacity",
     "flkb_batch_device_counts", "flkb_batch_device_features", "flkb_batch_device_stats",
     "flkb_batch_device_pyramid", "flkb_synth_frames_device", "flkb_kernel_launch_count",
-    "flkb_batch_kernels_per_run", "flkb_detector_responses"]
+    "flkb_batch_kernels_per_run", "flkb_detector_responses", "flkb_batch_run_device_timed"]
 
 _lib = None
 _vp = ctypes.c_void_p
@@ -167,6 +167,8 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
                                               ctypes.POINTER(ctypes.c_int),
                                               ctypes.POINTER(ctypes.c_size_t)]
     lib.flkb_detector_responses.argtypes = [_vp, _vp, _vp]
+    lib.flkb_batch_run_device_timed.argtypes = [_vp, _vp, ctypes.c_size_t, ctypes.c_int,
+                                                ctypes.c_int, _vp, _vp]
     lib.flkb_synth_frames_device.argtypes = [_vp, ctypes.c_int, ctypes.c_uint64, ctypes.c_int,
                                              ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                              ctypes.c_size_t, _vp]
@@ -371,6 +373,15 @@ class DeviceBatch(_Handle):
                    stream: int = 0, with_stats: bool = False) -> None:
         _check(_lib.flkb_batch_run_device(self._h, frames_ptr, frame_stride, row_pitch, count,
                                           int(with_stats), stream or None))
+
+    def run_device_timed(self, frames_ptr: int, frame_stride: int, row_pitch: int, count: int,
+                         stream: int = 0):
+        """Synchronous run; returns device microseconds of (pyramid, fused
+        detection, compaction) measured with CUDA events on `stream`."""
+        us = (ctypes.c_double * 3)()
+        _check(_lib.flkb_batch_run_device_timed(self._h, frames_ptr, frame_stride, row_pitch,
+                                                count, stream or None, us))
+        return tuple(us)
 
     def run_host(self, frames_ptr: int, frame_stride: int, row_pitch: int, count: int,
                  stream: int = 0) -> None:
