@@ -187,14 +187,24 @@ fused::Params fused_geometry(const DetectParams& p, const Geometry& g, int R, in
     L.cta0 = cta;
     cta += L.bands * L.tiles_x;
     tw_max = std::max(tw_max, L.tile_w);
+    L.nw = 1;
+    for (int t = 0; t < L.tiles_x; ++t) {  // the kernel's per-tile word count, maximised
+      const int x_lo = t * L.tile_w, x_hi = std::min(x_lo + L.tile_w, L.w);
+      const int bx0 = (x_lo - n - 3) & ~15;
+      L.nw = std::max(L.nw, (x_hi + n - bx0 - 3 + fused::kOwn - 1) / fused::kOwn);
+    }
+    L.div_nw = fused::FastDiv::make(static_cast<uint32_t>(L.nw));
+    L.div_tiles = fused::FastDiv::make(static_cast<uint32_t>(L.tiles_x));
     slots = std::max(slots, ((R << k) / p.cell_h + 2) * g.cols);
   }
-  P.nw_max = (tw_max + 2 * n + 15 + fused::kOwn - 1) / fused::kOwn;
+  P.nw_max = 1;
+  for (int k = 0; k < g.levels; ++k) P.nw_max = std::max(P.nw_max, P.lv[k].nw);
   P.sw = static_cast<int>(round_up(
       static_cast<size_t>(std::max(fused::kOwn * (P.nw_max - 1) + 36, tw_max + 2 * n + 22)), 16));
   P.rp = static_cast<int>(round_up(static_cast<size_t>(tw_max + 4 * n), 8));
   // 32-bit in-cell keys need cells of at most 1024 px per side
   P.key_slots = (p.cell_w <= 1024 && p.cell_h <= 1024 && slots <= 4096) ? slots : 0;
+  for (int i = 0; i < 32; ++i) P.pow2[i] = 1u << i;
   return P;
 }
 

@@ -70,6 +70,8 @@ struct Level {
   int bands;            // row bands of R rows
   int cta0;             // first blockIdx.x of this level
   int tma;              // rows may be fetched with cp.async.bulk
+  int nw;               // plane words per row (max over the level's tiles)
+  FastDiv div_nw, div_tiles;
 };
 
 struct Params {
@@ -82,6 +84,7 @@ struct Params {
   int nw_max;     // plane words per row, max over tiles
   int rp;         // score tile pitch (u16)
   int key_slots;  // shared cell-key capacity
+  uint32_t pow2[32];  // 1 << i, read from the constant bank so shifts can issue as IMAD
   unsigned long long* keys;
   unsigned long long* stats;
 };
@@ -145,6 +148,34 @@ __device__ __forceinline__ uint32_t lop3_xor3(uint32_t a, uint32_t b, uint32_t c
   asm("lop3.b32 %0, %1, %2, %3, 0x96;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
   return d;
 }
+// Shifts on the FMA pipe (IMAD), leaving the ALU pipe -- which issues at half
+// rate and carries every LOP3 -- to the bit-sliced logic:
+// x >> k = mulhi(x, 2^(32-k)); x << k = mullo(x, 2^k), with 2^k read from the
+// constant bank so ptxas cannot strength-reduce it back into SHF.
+template <int K>
+__device__ __forceinline__ uint32_t shr_fma(uint32_t x) {
+  uint32_t d;
+  asm("mul.hi.u32 %0, %1, %2;" : "=r"(d) : "r"(x), "n"(1u << (32 - K)));
+  return d;
+}
+__device__ __forceinline__ uint32_t shl_fma(uint32_t x, uint32_t pow2k) {
+  uint32_t d;
+  asm("mul.lo.u32 %0, %1, %2;" : "=r"(d) : "r"(x), "r"(pow2k));
+  return d;
+}
+// Ring-plane shift by a (compile-time after unrolling) dx in [-3, 3]: bit b
+// of the result holds bit b + dx of x.
+__device__ __forceinline__ uint32_t shift_fma(uint32_t x, int dx, const uint32_t (&pow2)[32]) {
+  switch (dx) {
+    case 1: return shr_fma<1>(x);
+    case 2: return shr_fma<2>(x);
+    case 3: return shr_fma<3>(x);
+    case -1: return shl_fma(x, pow2[1]);
+    case -2: return shl_fma(x, pow2[2]);
+    case -3: return shl_fma(x, pow2[3]);
+    default: return x;
+  }
+}
 __device__ __forceinline__ uint32_t and3(uint32_t a, uint32_t b, uint32_t c) { return a & b & c; }
 __device__ __forceinline__ uint32_t or3(uint32_t a, uint32_t b, uint32_t c) { return a | b | c; }
 
@@ -157,22 +188,23 @@ __device__ __forceinline__ uint32_t sliced_less(const uint32_t (&a)[8], const ui
 }
 
 // 32 pixels (8 words, pixel 4m+i in byte i of word m) -> 8 bit planes.
-__device__ __forceinline__ void transpose32x8(const uint32_t (&w)[8], uint32_t (&p)[8]) {
+__device__ __forceinline__ void transpose32x8(const uint32_t (&w)[8], uint32_t (&p)[8],
+                                              const uint32_t (&pow2)[32]) {
   uint32_t lo[4], hi[4];
 #pragma unroll
   for (int t = 0; t < 4; ++t) {
     uint32_t l = w[2 * t], h = w[2 * t + 1], x;
-    x = (l ^ (l >> 7)) & 0x00AA00AAu;
-    l = l ^ x ^ (x << 7);
-    x = (h ^ (h >> 7)) & 0x00AA00AAu;
-    h = h ^ x ^ (x << 7);
-    x = (l ^ (l >> 14)) & 0x0000CCCCu;
-    l = l ^ x ^ (x << 14);
-    x = (h ^ (h >> 14)) & 0x0000CCCCu;
-    h = h ^ x ^ (x << 14);
-    x = (l ^ (h << 4)) & 0xF0F0F0F0u;
+    x = (l ^ shr_fma<7>(l)) & 0x00AA00AAu;
+    l = l ^ x ^ shl_fma(x, pow2[7]);
+    x = (h ^ shr_fma<7>(h)) & 0x00AA00AAu;
+    h = h ^ x ^ shl_fma(x, pow2[7]);
+    x = (l ^ shr_fma<14>(l)) & 0x0000CCCCu;
+    l = l ^ x ^ shl_fma(x, pow2[14]);
+    x = (h ^ shr_fma<14>(h)) & 0x0000CCCCu;
+    h = h ^ x ^ shl_fma(x, pow2[14]);
+    x = (l ^ shl_fma(h, pow2[4])) & 0xF0F0F0F0u;
     l ^= x;
-    h ^= x >> 4;
+    h ^= shr_fma<4>(x);
     lo[t] = l;
     hi[t] = h;
   }
@@ -241,10 +273,10 @@ __device__ __forceinline__ int sad_b_packed(const uint32_t (&r)[4], uint32_t c, 
 // without a division per step.
 struct TaskIter {
   int row, j, drow, dj, nw;
-  __device__ __forceinline__ TaskIter(int t0, int nw_) : nw(nw_) {
-    row = t0 / nw_;
+  __device__ __forceinline__ TaskIter(int t0, int nw_, const FastDiv& div) : nw(nw_) {
+    row = div(t0);
     j = t0 - row * nw_;
-    drow = kThreads / nw_;
+    drow = div(kThreads);
     dj = kThreads - drow * nw_;
   }
   __device__ __forceinline__ void next() {
@@ -268,7 +300,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_detect(const __grid_co
   while (k + 1 < P.levels && static_cast<int>(blockIdx.x) >= P.lv[k + 1].cta0) ++k;
   const Level& L = P.lv[k];
   const int local = blockIdx.x - L.cta0;
-  const int band = local / L.tiles_x, tile = local % L.tiles_x;
+  const int band = L.div_tiles(local), tile = local - band * L.tiles_x;
   const int f = blockIdx.y;
   const int n = RADIUS > 0 ? RADIUS : P.radius, w = L.w, h = L.h;
   const int y0 = band * P.R, y1 = min(y0 + P.R, h);          // rows suppressed here
@@ -277,7 +309,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_detect(const __grid_co
   const int iy0 = fy0 - 3;                                      // stage row 0 <-> image row iy0
   const int ya = max(iy0, 0), yb = min(y1 + n + 3, h);          // rows present in the stage
   const int bx0 = (x_lo - n - 3) & ~15;                         // stage column 0 <-> image x bx0
-  const int nw = (x_hi + n - bx0 - 3 + kOwn - 1) / kOwn;        // plane words per row
+  const int nw = L.nw;                                          // plane words per row
   const int cx_lo = max(x_lo - n, 3), cx_hi = min(x_hi + n, w - 3);  // FAST columns
   const int cy_lo = max(fy0, 3), cy_hi = min(y1 + n, h - 3);         // FAST rows
 
@@ -351,7 +383,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_detect(const __grid_co
   // --- 2. bit planes of every staged row
   {
     const int tasks = (yb - ya) * nw;
-    TaskIter it(tid, nw);
+    TaskIter it(tid, nw, L.div_nw);
     for (int t = tid; t < tasks; t += kThreads, it.next()) {
       const int r = ya - iy0 + it.row, j = it.j;
       const int bx = kOwn * j;
@@ -362,7 +394,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_detect(const __grid_co
       const uint32_t sel = (bx & 2) ? 0x5432u : 0x3210u;
 #pragma unroll
       for (int i = 0; i < 8; ++i) wv[i] = __byte_perm(a[i], a[i + 1], sel);
-      transpose32x8(wv, pl);
+      transpose32x8(wv, pl, P.pow2);
       uint32_t* dst = planes + (r * P.nw_max + j) * 4;
       *reinterpret_cast<uint4*>(dst) = make_uint4(pl[0], pl[1], pl[2], pl[3]);
       *reinterpret_cast<uint4*>(dst + half) = make_uint4(pl[4], pl[5], pl[6], pl[7]);
@@ -377,7 +409,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_detect(const __grid_co
 #pragma unroll
     for (int b = 0; b < 8; ++b) E[b] = ((P.eps >> b) & 1) ? 0xFFFFFFFFu : 0u;
     const int tasks = max(fast_rows, 0) * nw;
-    TaskIter it(tid, nw);
+    TaskIter it(tid, nw, L.div_nw);
     for (int t = tid; t < tasks; t += kThreads, it.next()) {
       const int y = cy_lo + it.row, j = it.j;
       const int r = y - iy0;  // stage/plane row of the centre
@@ -417,7 +449,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_detect(const __grid_co
           const int dx = ring_dx(i);
           uint32_t s[8];
 #pragma unroll
-          for (int b = 0; b < 8; ++b) s[b] = dx > 0 ? (q[b] >> dx) : dx < 0 ? (q[b] << -dx) : q[b];
+          for (int b = 0; b < 8; ++b) s[b] = shift_fma(q[b], dx, P.pow2);
           dk[i] = sliced_less(s, lo);
           bk[i] = sliced_less(hi, s);
         }
@@ -470,7 +502,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_detect(const __grid_co
   const int base = scan[warp] + incl - cnt;  // this thread's first list index
   const int total = scan[kWarps];
   const int cap = list_capacity(P);
-  const int row_tb = tb / nw, j_tb = tb - row_tb * nw;
+  const int row_tb = L.div_nw(tb), j_tb = tb - row_tb * nw;
   // Writes the entries with list index in [w0, w0 + cap) to list[index - w0].
   auto build = [&](int w0) {
     if (total <= cap) {
