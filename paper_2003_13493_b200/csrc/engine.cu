@@ -159,12 +159,9 @@ namespace {
 constexpr int kFusedSmemTarget = (228 * 1024) / fused::kMinBlocks - 1024;
 constexpr int kFusedSmemMax = 227 * 1024;
 
-// Launch geometry of the fused kernel: bands of R rows, column tiles (all
-// levels share one shared-memory layout), and row segments -- one CTA walks
-// the bands of one segment, so segments trade halo recompute (2n+6 rows per
-// segment) for parallelism; `count` frames get ~2 waves of CTAs.
-fused::Params fused_geometry(const DetectParams& p, const Geometry& g, int R, int tiles0,
-                             int count) {
+// Shared-memory geometry of the fused kernel for column tiles of at most
+// `tile_w` pixels (every level uses the same layout).
+fused::Params fused_geometry(const DetectParams& p, const Geometry& g, int R, int tiles0) {
   fused::Params P{};
   P.levels = g.levels;
   P.eps = p.epsilon;
@@ -178,9 +175,6 @@ fused::Params fused_geometry(const DetectParams& p, const Geometry& g, int R, in
   P.cells = g.cells;
   const int n = p.radius;
   int tw_max = 1, slots = 0, cta = 0;
-  size_t px_total = 0;
-  for (int k = 0; k < g.levels; ++k) px_total += static_cast<size_t>(g.lw[k]) * g.lh[k];
-  const int want_ctas = std::max(1, (2 * 148 * fused::kMinBlocks + count - 1) / count);
   for (int k = 0; k < g.levels; ++k) {
     fused::Level& L = P.lv[k];
     L.w = g.lw[k];
@@ -189,13 +183,9 @@ fused::Params fused_geometry(const DetectParams& p, const Geometry& g, int R, in
     L.tiles_x = std::max(std::max(1, std::min(tiles0, (L.w + 63) / 64)), (L.w + 927) / 928);
     L.tile_w = (L.w + L.tiles_x - 1) / L.tiles_x;
     L.tiles_x = (L.w + L.tile_w - 1) / L.tile_w;
-    const int bands = (L.h + R - 1) / R;
-    const double share = static_cast<double>(L.w) * L.h / static_cast<double>(px_total);
-    const int segs = std::max(1, std::min(bands, static_cast<int>(want_ctas * share / L.tiles_x + 0.5)));
-    L.seg_rows = (bands + segs - 1) / segs * R;
-    L.segs = (L.h + L.seg_rows - 1) / L.seg_rows;
+    L.bands = (L.h + R - 1) / R;
     L.cta0 = cta;
-    cta += L.segs * L.tiles_x;
+    cta += L.bands * L.tiles_x;
     tw_max = std::max(tw_max, L.tile_w);
     L.nw = 1;
     for (int t = 0; t < L.tiles_x; ++t) {  // the kernel's per-tile word count, maximised
@@ -214,17 +204,8 @@ fused::Params fused_geometry(const DetectParams& p, const Geometry& g, int R, in
   P.rp = static_cast<int>(round_up(static_cast<size_t>(tw_max + 4 * n), 8));
   // 32-bit in-cell keys need cells of at most 1024 px per side
   P.key_slots = (p.cell_w <= 1024 && p.cell_h <= 1024 && slots <= 4096) ? slots : 0;
-  // corner list: the worst case of a band, capped (a denser band is scored in rounds)
-  const int worst = (R + 2 * n) * P.nw_max * fused::kOwn;
-  P.list_cap = static_cast<int>(round_up(static_cast<size_t>(std::min(worst, 4096)), 8));
   for (int i = 0; i < 32; ++i) P.pow2[i] = 1u << i;
   return P;
-}
-
-int fused_ctas(const fused::Params& P) {
-  int c = 0;
-  for (int k = 0; k < P.levels; ++k) c += P.lv[k].segs * P.lv[k].tiles_x;
-  return c;
 }
 
 }  // namespace
@@ -237,21 +218,19 @@ void DeviceBatch::run(const uint8_t* frames, size_t fstride, int pitch, int coun
   if (pitch < g_.width) throw InvalidArgument("row pitch smaller than the frame width");
   if (count > 65535) throw InvalidArgument("at most 65535 frames per launch");
   DeviceGuard guard(device_);
-  // bands carry a 2n+6-row halo into the next band: R >= 2n+6
-  const int r_min = std::max(8, 2 * p_.radius + 6);
-  int R = std::max(fused_R_, r_min);
+  int R = fused_R_;
   const char* forced = std::getenv("FLKB_BAND_ROWS");  // tuning override
-  if (forced) R = std::max(r_min, std::atoi(forced));
+  if (forced) R = std::max(4, std::atoi(forced));
   int tiles0 = 1;
-  fused::Params P = fused_geometry(p_, g_, R, tiles0, count);
+  fused::Params P = fused_geometry(p_, g_, R, tiles0);
   // shrink the band until kMinBlocks CTAs fit one SM, then split columns
-  while (!forced && fused::smem_layout(P).total > kFusedSmemTarget && R - 4 >= r_min) {
+  while (!forced && fused::smem_layout(P).total > kFusedSmemTarget && R > 16) {
     R -= 4;
-    P = fused_geometry(p_, g_, R, tiles0, count);
+    P = fused_geometry(p_, g_, R, tiles0);
   }
   while (fused::smem_layout(P).total > kFusedSmemTarget && P.lv[0].tile_w > 64) {
     ++tiles0;
-    P = fused_geometry(p_, g_, R, tiles0, count);
+    P = fused_geometry(p_, g_, R, tiles0);
   }
   const int smem = fused::smem_layout(P).total;
   if (smem > kFusedSmemMax) {  // pathological radius / geometry: staged kernels
@@ -289,7 +268,7 @@ void DeviceBatch::run(const uint8_t* frames, size_t fstride, int pitch, int coun
     ++launched;
   }
   if (times) check_cuda(cudaEventRecord(ev[1], s), "cudaEventRecord");
-  const int ctas = fused_ctas(P);
+  int ctas = 0;
   for (int k = 0; k < g_.levels; ++k) {
     fused::Level& L = P.lv[k];
     L.img = k == 0 ? frames : pyr + g_.loff[k];
@@ -297,6 +276,7 @@ void DeviceBatch::run(const uint8_t* frames, size_t fstride, int pitch, int coun
     L.fstride = k == 0 ? fstride : g_.pyr_frame_bytes;
     L.tma = (reinterpret_cast<uintptr_t>(L.img) % 16 == 0) && L.pitch % 16 == 0 &&
             L.fstride % 16 == 0;
+    ctas += L.bands * L.tiles_x;
   }
   P.keys = keys;
   P.stats = stats ? st : nullptr;
