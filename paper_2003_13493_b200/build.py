@@ -42,7 +42,8 @@ def _deps() -> float:
 
 def _compile(src: str, verbose: bool) -> str:
     obj = os.path.join(OBJ, os.path.basename(src) + ".o")
-    cmd = [nvcc()] + ARCH + COMMON + ["-c", src, "-o", obj]
+    cmd = [nvcc()] + ARCH + COMMON + os.environ.get("FLKB_NVCC_FLAGS", "").split() + [
+        "-c", src, "-o", obj]
     if src.endswith(".cu"):
         cmd += ["-Xptxas", "-v"] if verbose else []
         cmd += ["--expt-relaxed-constexpr"]

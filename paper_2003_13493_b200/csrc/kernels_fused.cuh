@@ -90,7 +90,7 @@ struct Params {
 };
 
 struct Smem {
-  int stage, planes, cm, list, scan, skeys, bar, total;
+  int stage, planes, cm, list, scan, skeys, lut, bar, total;
 };
 
 // Corner-list capacity (u16 entries); a band with more corners is scored in
@@ -124,6 +124,9 @@ __host__ __device__ inline Smem smem_layout(const Params& p) {
   off = (off + 15) & ~15;
   s.skeys = off;
   off += p.key_slots * 4;
+  off = (off + 15) & ~15;
+  s.lut = off;  // colkey[sw], rowkey[fast_rows]
+  off += p.key_slots > 0 ? (p.sw + fast_rows) * 4 : 0;
   off = (off + 15) & ~15;
   s.bar = off;
   off += 16;
@@ -319,7 +322,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_detect(const __grid_co
   uint32_t* cm = reinterpret_cast<uint32_t*>(smem + S.cm);
   uint16_t* list = reinterpret_cast<uint16_t*>(smem + S.list);
   int* scan = reinterpret_cast<int*>(smem + S.scan);
-  uint32_t* colkey = reinterpret_cast<uint32_t*>(stage);  // live once scoring is done
+  uint32_t* colkey = reinterpret_cast<uint32_t*>(smem + S.lut);
   uint32_t* rowkey = colkey + P.sw;
   // planes: low half (bit planes 0-3) and high half (4-7) in separate arrays
   // so a warp's 16-byte accesses to consecutive words are bank-conflict free
@@ -496,11 +499,42 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_detect(const __grid_co
       if (lane >= o) acc += u;
     }
     if (lane < kWarps) scan[lane] = acc - v;
-    if (lane == 31) scan[kWarps] = acc;
+    if (lane == 31) scan[kWarps] = scan[kWarps + 1] = scan[kWarps + 2] = acc;
+  }
+  // In-cell key parts per stage column and per tile row: colkey = cell_x << 10
+  // | (1023 - local x), rowkey = slot row base << 10 | (1023 - local y); a
+  // survivor's key and slot are then two loads away.
+  if (local_keys) {
+    for (int xs = tid; xs < P.sw; xs += kThreads) {
+      const int x = max(bx0 + xs, 0);
+      const int ccx = P.div_cw(x << k);
+      const int ox = (ccx * P.cell_w + (1 << k) - 1) >> k;
+      colkey[xs] = (static_cast<uint32_t>(ccx) << 10) | ((1023u - (x - ox)) & 1023u);
+    }
+    for (int r = tid; r < fast_rows; r += kThreads) {
+      const int y = cy_lo + r;
+      const int ccy = P.div_ch(y << k);
+      const int oy = (ccy * P.cell_h + (1 << k) - 1) >> k;
+      rowkey[r] = (static_cast<uint32_t>(max(ccy - cr0, 0) * P.cols) << 10) |
+                  ((1023u - (y - oy)) & 1023u);
+    }
   }
   __syncthreads();
   const int base = scan[warp] + incl - cnt;  // this thread's first list index
   const int total = scan[kWarps];
+  // List range of the suppressed rows [y0, y1): tasks [T0, T1) are row-major,
+  // so their corners are entries [e_lo, e_hi); the owner of task T records
+  // its list index (read after the scoring barrier).
+  const int T0 = min(max(max(y0, 3) - cy_lo, 0) * nw, tasks_f);
+  const int T1 = min(max(min(y1, h - 3) - cy_lo, 0) * nw, tasks_f);
+  if (tb < te) {
+    int pos = base;
+    for (int t = tb; t < te; ++t) {
+      if (t == T0) scan[kWarps + 1] = pos;
+      if (t == T1) scan[kWarps + 2] = pos;
+      pos += __popc(cm[t]);
+    }
+  }
   const int cap = list_capacity(P);
   const int row_tb = L.div_nw(tb), j_tb = tb - row_tb * nw;
   // Writes the entries with list index in [w0, w0 + cap) to list[index - w0].
@@ -601,40 +635,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_detect(const __grid_co
   //        a contiguous range of the list, since tasks are row-major
   unsigned long long n_cand = 0, n_cmp = 0;
   {
-    const int ny_lo = max(y0, 3), ny_hi = min(y1, h - 3);
     const int nx_lo = max(x_lo, 3), nx_hi = min(x_hi, w - 3);
-    const int T0 = min(max(ny_lo - cy_lo, 0) * nw, tasks_f);
-    const int T1 = min(max(ny_hi - cy_lo, 0) * nw, tasks_f);
-    // list index of task T: the owning thread's base + corners before T
-    if (tid == 0) scan[kWarps + 1] = scan[kWarps + 2] = total;
-    __syncthreads();
-    if (tb < te) {
-      int pos = base;
-      for (int t = tb; t < te; ++t) {
-        if (t == T0) scan[kWarps + 1] = pos;
-        if (t == T1) scan[kWarps + 2] = pos;
-        pos += __popc(cm[t]);
-      }
-    }
-    // In-cell key parts per stage column and per tile row, in the dead stage:
-    // colkey = cell_x << 10 | (1023 - local x), rowkey = slot row base << 10 |
-    // (1023 - local y). A survivor's key and slot are then two loads away.
-    if (local_keys) {
-      for (int xs = tid; xs < P.sw; xs += kThreads) {
-        const int x = max(bx0 + xs, 0);
-        const int ccx = P.div_cw(x << k);
-        const int ox = (ccx * P.cell_w + (1 << k) - 1) >> k;
-        colkey[xs] = (static_cast<uint32_t>(ccx) << 10) | ((1023u - (x - ox)) & 1023u);
-      }
-      for (int r = tid; r < fast_rows; r += kThreads) {
-        const int y = cy_lo + r;
-        const int ccy = P.div_ch(y << k);
-        const int oy = (ccy * P.cell_h + (1 << k) - 1) >> k;
-        rowkey[r] = (static_cast<uint32_t>(max(ccy - cr0, 0) * P.cols) << 10) |
-                    ((1023u - (y - oy)) & 1023u);
-      }
-    }
-    __syncthreads();
     const int e_lo = T1 > T0 ? scan[kWarps + 1] : 0;
     const int e_hi = T1 > T0 ? scan[kWarps + 2] : 0;
     const int rp = P.rp;
