@@ -90,6 +90,22 @@ class ClockSampler:
         self._t = None
 
     def _run(self):
+        try:  # NVML directly: ~1 ms per sample instead of a process per sample
+            import pynvml as nv
+            nv.nvmlInit()
+            hnd = nv.nvmlDeviceGetHandleByIndex(self.device)
+            mx = nv.nvmlDeviceGetMaxClockInfo(hnd, nv.NVML_CLOCK_SM)
+            bits = [nv.nvmlClocksEventReasonHwSlowdown, nv.nvmlClocksEventReasonHwThermalSlowdown,
+                    nv.nvmlClocksEventReasonSwThermalSlowdown, nv.nvmlClocksEventReasonSwPowerCap]
+            while not self._stop.is_set():
+                sm = nv.nvmlDeviceGetClockInfo(hnd, nv.NVML_CLOCK_SM)
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(hnd)
+                self.samples.append([str(sm), str(mx)] +
+                                    ["Active" if r & b else "Not Active" for b in bits])
+                self._stop.wait(0.05)
+            return
+        except Exception:
+            self.samples.clear()
         while not self._stop.is_set():
             try:
                 out = subprocess.run(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
@@ -181,7 +197,7 @@ def run_reference_arm(args, rank: int, world: int):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--batch", type=int, default=4096, help="frames per GPU per step")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])

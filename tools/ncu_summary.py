@@ -52,7 +52,7 @@ def main():
     a = ap.parse_args()
     kernels, units = raw_metrics(a.report)
     keys = ["gpu__time_duration.sum", "sm__throughput.avg.pct_of_peak_sustained_elapsed",
-            "sm__inst_executed.sum", "smsp__thread_inst_executed.sum",
+            "smsp__inst_executed.sum", "smsp__thread_inst_executed_per_inst_executed.ratio",
             "sm__instruction_throughput.avg.pct_of_peak_sustained_active",
             "smsp__issue_active.avg.pct_of_peak_sustained_active",
             "sm__warps_active.avg.pct_of_peak_sustained_active", "launch__registers_per_thread",
@@ -67,10 +67,10 @@ def main():
             if m in k:
                 print(f"  {m:62s} {k[m]:>18s} {units.get(m, '')}")
         if a.pixels_per_launch:
-            ti = float(k.get("smsp__thread_inst_executed.sum", "0").replace(",", ""))
-            wi = float(k.get("sm__inst_executed.sum", "0").replace(",", ""))
-            print(f"  thread instructions / pixel {ti / a.pixels_per_launch:10.1f}")
-            print(f"  warp-instr slots / pixel x32 {32 * wi / a.pixels_per_launch:10.1f}")
+            wi = float(k.get("smsp__inst_executed.sum", "0").replace(",", ""))
+            tr = float(k.get("smsp__thread_inst_executed_per_inst_executed.ratio", "0").replace(",", ""))
+            print(f"  warp instructions / pixel      {wi / a.pixels_per_launch:10.3f}")
+            print(f"  thread instructions / pixel    {wi * tr / a.pixels_per_launch:10.1f}")
     agg = source_lines(a.report)
     tot = sum(v[0] for v in agg.values()) or 1
     ts = sum(v[1] for v in agg.values()) or 1
