@@ -72,6 +72,7 @@ struct Level {
   int tma;              // rows may be fetched with cp.async.bulk
   int nw;               // plane words per row (max over the level's tiles)
   FastDiv div_nw, div_tiles;
+  int kt_col, kt_row;   // offsets of this level's column / row key tables in keytab
 };
 
 struct Params {
@@ -85,12 +86,16 @@ struct Params {
   int rp;         // score tile pitch (u16)
   int key_slots;  // shared cell-key capacity
   uint32_t pow2[32];  // 1 << i, read from the constant bank so shifts can issue as IMAD
+  uint32_t emask[8];  // ~0 where bit b of eps is set
+  // In-cell key tables (DeviceBatch::keytab): per level, for every column x
+  // cell_x << 10 | (1023 - (x - first x of the cell)), then likewise per row.
+  const uint32_t* keytab;
   unsigned long long* keys;
   unsigned long long* stats;
 };
 
 struct Smem {
-  int stage, planes, cm, list, scan, skeys, lut, bar, total;
+  int stage, planes, cm, list, scan, skeys, bar, total;
 };
 
 // Corner-list capacity (u16 entries); a band with more corners is scored in
@@ -124,9 +129,6 @@ __host__ __device__ inline Smem smem_layout(const Params& p) {
   off = (off + 15) & ~15;
   s.skeys = off;
   off += p.key_slots * 4;
-  off = (off + 15) & ~15;
-  s.lut = off;  // colkey[sw], rowkey[fast_rows]
-  off += p.key_slots > 0 ? (p.sw + fast_rows) * 4 : 0;
   off = (off + 15) & ~15;
   s.bar = off;
   off += 16;
@@ -322,8 +324,6 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_detect(const __grid_co
   uint32_t* cm = reinterpret_cast<uint32_t*>(smem + S.cm);
   uint16_t* list = reinterpret_cast<uint16_t*>(smem + S.list);
   int* scan = reinterpret_cast<int*>(smem + S.scan);
-  uint32_t* colkey = reinterpret_cast<uint32_t*>(smem + S.lut);
-  uint32_t* rowkey = colkey + P.sw;
   // planes: low half (bit planes 0-3) and high half (4-7) in separate arrays
   // so a warp's 16-byte accesses to consecutive words are bank-conflict free
   const int half = (P.R + 2 * n + 6) * P.nw_max * 4;
@@ -408,9 +408,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_detect(const __grid_co
   // --- 3. bit-sliced corner masks for the FAST rows
   const int fast_rows = cy_hi - cy_lo;
   {
-    uint32_t E[8];
-#pragma unroll
-    for (int b = 0; b < 8; ++b) E[b] = ((P.eps >> b) & 1) ? 0xFFFFFFFFu : 0u;
+    const uint32_t (&E)[8] = P.emask;  // eps bit masks, constant-bank operands
     const int tasks = max(fast_rows, 0) * nw;
     TaskIter it(tid, nw, L.div_nw);
     for (int t = tid; t < tasks; t += kThreads, it.next()) {
@@ -430,10 +428,11 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_detect(const __grid_co
         uint32_t br = 0, cy = 0;
 #pragma unroll
         for (int b = 0; b < 8; ++b) {
-          lo[b] = lop3_xor3(c[b], E[b], br);
-          br = lop3_maj_na(c[b], E[b], br);
-          hi[b] = lop3_xor3(c[b], E[b], cy);
-          cy = lop3_maj(c[b], E[b], cy);
+          // plain C so ptxas can take E[b] straight from the constant bank
+          lo[b] = c[b] ^ E[b] ^ br;
+          br = (~c[b] & E[b]) | (~c[b] & br) | (E[b] & br);
+          hi[b] = c[b] ^ E[b] ^ cy;
+          cy = (c[b] & E[b]) | (c[b] & cy) | (E[b] & cy);
         }
 #pragma unroll
         for (int b = 0; b < 8; ++b) {
@@ -500,24 +499,6 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_detect(const __grid_co
     }
     if (lane < kWarps) scan[lane] = acc - v;
     if (lane == 31) scan[kWarps] = scan[kWarps + 1] = scan[kWarps + 2] = acc;
-  }
-  // In-cell key parts per stage column and per tile row: colkey = cell_x << 10
-  // | (1023 - local x), rowkey = slot row base << 10 | (1023 - local y); a
-  // survivor's key and slot are then two loads away.
-  if (local_keys) {
-    for (int xs = tid; xs < P.sw; xs += kThreads) {
-      const int x = max(bx0 + xs, 0);
-      const int ccx = P.div_cw(x << k);
-      const int ox = (ccx * P.cell_w + (1 << k) - 1) >> k;
-      colkey[xs] = (static_cast<uint32_t>(ccx) << 10) | ((1023u - (x - ox)) & 1023u);
-    }
-    for (int r = tid; r < fast_rows; r += kThreads) {
-      const int y = cy_lo + r;
-      const int ccy = P.div_ch(y << k);
-      const int oy = (ccy * P.cell_h + (1 << k) - 1) >> k;
-      rowkey[r] = (static_cast<uint32_t>(max(ccy - cr0, 0) * P.cols) << 10) |
-                  ((1023u - (y - oy)) & 1023u);
-    }
   }
   __syncthreads();
   const int base = scan[warp] + incl - cnt;  // this thread's first list index
@@ -694,9 +675,11 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_detect(const __grid_co
         }
         if (!keep) continue;
         if (local_keys) {
-          const uint32_t ck = colkey[xs], rk = rowkey[y - cy_lo];
+          // in-cell key parts from the level's table: cell << 10 | (1023 - local)
+          const uint32_t ck = __ldg(P.keytab + L.kt_col + x), rk = __ldg(P.keytab + L.kt_row + y);
           const uint32_t key = (static_cast<uint32_t>(s) << 20) | ((rk & 1023u) << 10) | (ck & 1023u);
-          atomicMax(skeys + (rk >> 10) + (ck >> 10), key);
+          atomicMax(skeys + (static_cast<int>(rk >> 10) - cr0) * P.cols + static_cast<int>(ck >> 10),
+                    key);
         } else {
           const int X = x << k, Y = y << k;
           atomicMax(P.keys + static_cast<size_t>(f) * P.cells + P.div_ch(Y) * P.cols + P.div_cw(X),
