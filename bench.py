@@ -157,6 +157,65 @@ def cpu_reference(frames_n: int, workers: int):
             "features": int(feats)}
 
 
+def other_configs(device: int):
+    """BASELINE configs other than the headline one, measured on this GPU
+    (reported beside the headline, not as it): C2 single-frame latency
+    through the C ABI, C3 and C5 batch throughput on device-resident frames."""
+    import torch
+    import paper_2003_13493_b200 as fl
+    out = {}
+    # C2: one 752x480 frame per flk_detector_run (CUDA-graph replay: H2D,
+    # 4 kernels, D2H of the feature list), host wall time per call
+    det = fl.Detector(fl.Config(**CFG), device=device)
+    img = fl.Image.from_array(np.ascontiguousarray(
+        torch.empty((H, W), dtype=torch.uint8).random_(0, 256).numpy()))
+    for _ in range(20):
+        det.run(img)
+    ts = []
+    for _ in range(300):
+        t0 = time.perf_counter()
+        det.run(img)
+        ts.append(time.perf_counter() - t0)
+    ts = np.array(ts) * 1e6
+    out["C2_latency"] = {"workload": "752x480 l=3 FAST-9 sad_b, 1 frame via flk_detector_run",
+                         "e2e_us_median": float(np.median(ts)), "e2e_us_p95": float(np.percentile(ts, 95)),
+                         "includes": "pinned staging copy, H2D, pyramid+fused+compact kernels, D2H, "
+                                     "feature list build"}
+
+    def batch_fps(cfg, w, h, frames, cell=None, steps=10):
+        c = fl.Config(**cfg)
+        if cell:
+            c.set_cell_size_px(*cell)
+        d = fl.Detector(c, device=device)
+        b = fl.DeviceBatch(d, w, h, frames)
+        pitch = (w + 15) // 16 * 16
+        buf = torch.empty((frames, h, pitch), dtype=torch.uint8, device="cuda")
+        st = torch.cuda.current_stream().cuda_stream
+        fl.synth_frames_device(buf.data_ptr(), 1, 0, frames, w, h, pitch, pitch * h, st)
+        for _ in range(3):
+            b.run_device(buf.data_ptr(), pitch * h, pitch, frames, st)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(steps):
+            b.run_device(buf.data_ptr(), pitch * h, pitch, frames, st)
+        e1.record()
+        torch.cuda.synchronize()
+        fps = frames * steps / (e0.elapsed_time(e1) / 1e3)
+        del buf
+        return fps
+
+    c3 = dict(epsilon=10, N=12, score_kind="sad_b", l=4, w=1, h=2, n=1)
+    fps = batch_fps(c3, 1920, 1080, 256, cell=(16, 16))
+    out["C3"] = {"workload": "1920x1080 l=4 FAST-12 sad_b, 16x16 cells (extension), batch 256, "
+                             "S2 frames on device", "frames_per_s": fps, "mpix_per_s": fps * 1920 * 1080 / 1e6}
+    c5 = dict(epsilon=10, N=10, score_kind="sad_b", l=5, w=1, h=2, n=1)
+    fps = batch_fps(c5, 3840, 2160, 64)
+    out["C5_1gpu"] = {"workload": "3840x2160 l=5 FAST-10 sad_b, 32x32 cells (w=1,h=2), batch 64, "
+                                  "S2 frames on device (per-GPU; the 8-GPU line is the weak-scaling run)",
+                      "frames_per_s": fps, "mpix_per_s": fps * 3840 * 2160 / 1e6}
+    return out
+
+
 def run_reference_arm(args, rank: int, world: int):
     if rank != 0:
         return
@@ -203,6 +262,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extras", action="store_true", help="skip the C2/C3/C5 side lines")
     args = ap.parse_args()
 
     rank = int(os.environ.get("RANK", "0"))
@@ -332,6 +392,8 @@ def main():
             "gpu_launches": int(launches),
             "clocks": clocks.summary(),
         }
+        if not args.no_extras and world == 1:
+            line["other_configs"] = other_configs(local)
         if not args.no_cpu_baseline and world == 1:
             workers = os.cpu_count() or 1
             line["cpu_baseline"] = cpu_reference(min(4096, max(512, 128 * workers)), workers)

@@ -209,3 +209,66 @@ def test_repeatable_and_launch_counted():
     b = det.run(img)
     assert (a == b).all()
     assert fl.kernel_launch_count() > before
+
+
+def test_unaligned_pitch_uses_plain_loads_and_matches(orc):
+    """Level 0 with a 753-byte pitch cannot use cp.async.bulk: the fused
+    kernel's plain-load staging path must give the same features."""
+    import torch
+    W, H, n = 753, 481, 5
+    cfg = dict(epsilon=10, N=9, score_kind="sad_b", l=3, w=1, h=8, n=1)
+    frames = np.stack([synth.texture(30 + f, W, H) for f in range(n)])
+    det = fl.Detector(make_config(cfg))
+    batch = fl.DeviceBatch(det, W, H, n)
+    d = torch.from_numpy(frames).cuda()
+    batch.run_device(d.data_ptr(), W * H, W, n)
+    torch.cuda.synchronize()
+    res = batch.results(n)
+    p = oracle.make_params(**cfg)
+    for f in range(n):
+        ref, _ = orc.detect(frames[f], p)
+        assert (res[f] == ref).all()
+
+
+@pytest.mark.parametrize("kind", ["sad_b", "sad_a"])
+def test_dense_corners_multi_round_list(orc, kind):
+    """eps = 0 on noise makes most pixels corners, overflowing the shared
+    corner list: the kernel scores and suppresses in several rounds."""
+    img = synth.noise(77, 752, 480)
+    cfg = dict(epsilon=0, N=9, score_kind=kind, l=2, w=1, h=16, n=1)
+    feats, extra = fl.Detector(make_config(cfg)).run(img, stats=True)
+    ref, st = orc.detect(img, oracle.make_params(**cfg))
+    assert (feats == ref).all()
+    assert extra["stats"]["nms_candidates"] == st.candidates
+    assert st.candidates > 200_000  # genuinely dense
+
+
+@pytest.mark.parametrize("n", [2, 3, 4])
+def test_radius_generic_path_large_frames(orc, n):
+    img = synth.texture(5, 1280, 720)
+    cfg = dict(epsilon=12, N=10, score_kind="sad_b", l=3, w=2, h=4, n=n)
+    feats = fl.Detector(make_config(cfg)).run(img)
+    ref, _ = orc.detect(img, oracle.make_params(**cfg))
+    assert (feats == ref).all()
+
+
+def test_batch_api_with_stats_matches_single_runs():
+    frames = [synth.noise(40 + f, 320, 240) for f in range(4)]
+    cfg = dict(epsilon=10, N=9, score_kind="mt", l=2, w=1, h=16, n=1)
+    det = fl.Detector(make_config(cfg))
+    single = [fl.Detector(make_config(cfg)).run(f, stats=True) for f in frames]
+    lib = fl.load_library()
+    import ctypes
+    from paper_2003_13493_b200 import fastlk as fk
+    imgs = [fl.Image.from_array(f) for f in frames]
+    arr = (ctypes.c_void_p * 4)(*[i.handle.value for i in imgs])
+    outs = (ctypes.c_void_p * 4)()
+    stats = (fk.FrameStats * 4)()
+    assert lib.flkb_detector_run_batch(det.handle, arr, 4, outs, stats) == 0
+    for i in range(4):
+        h = ctypes.c_void_p(outs[i])
+        got = fk._features_to_array(h)
+        lib.flk_features_destroy(h)
+        assert (got == single[i][0]).all()
+        assert stats[i].nms_candidates == single[i][1]["stats"]["nms_candidates"]
+        assert stats[i].nms_comparisons == single[i][1]["stats"]["nms_comparisons"]

@@ -4,7 +4,7 @@
 mkdir -p gpurun_out
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
   --log-file gpurun_out/launches.csv python bench.py --batch 4096 --steps 2 --warmup 3 \
-  --e2e-steps 1 --no-cpu-baseline > gpurun_out/ncu_launch.log 2>&1
+  --e2e-steps 1 --no-cpu-baseline --no-extras > gpurun_out/ncu_launch.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_detect -s 3 -c 1 \
   -o gpurun_out/prof_full python bench.py --batch 4096 --steps 1 --warmup 3 --e2e-steps 1 \
   --no-cpu-baseline > gpurun_out/ncu_full.log 2>&1
