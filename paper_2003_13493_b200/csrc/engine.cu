@@ -227,6 +227,7 @@ fused::Params fused_geometry(const DetectParams& p, const Geometry& g, int R, in
   P.key_slots = (p.cell_w <= 1024 && p.cell_h <= 1024 && slots <= 4096) ? slots : 0;
   for (int i = 0; i < 32; ++i) P.pow2[i] = 1u << i;
   for (int b = 0; b < 8; ++b) P.emask[b] = ((p.epsilon >> b) & 1) ? 0xFFFFFFFFu : 0u;
+  if (const char* e = std::getenv("FLKB_LIST_CAP")) P.list_cap = std::max(256, std::atoi(e));
   return P;
 }
 
@@ -241,6 +242,7 @@ void DeviceBatch::run(const uint8_t* frames, size_t fstride, int pitch, int coun
   if (count > 65535) throw InvalidArgument("at most 65535 frames per launch");
   DeviceGuard guard(device_);
   int R = fused_R_;
+  const int r_min = 8;
   const char* forced = std::getenv("FLKB_BAND_ROWS");  // tuning override
   if (forced) R = std::max(4, std::atoi(forced));
   int tiles0 = 1;
@@ -251,6 +253,21 @@ void DeviceBatch::run(const uint8_t* frames, size_t fstride, int pitch, int coun
     P = fused_geometry(p_, g_, R, tiles0);
   }
   while (fused::smem_layout(P).total > kFusedSmemTarget && P.lv[0].tile_w > 64) {
+    ++tiles0;
+    P = fused_geometry(p_, g_, R, tiles0);
+  }
+  // Small batches (the single-frame latency path): trade halo work for
+  // parallelism until the grid covers the GPU.
+  auto ctas_of = [&](const fused::Params& q) {
+    int c = 0;
+    for (int k = 0; k < q.levels; ++k) c += q.lv[k].bands * q.lv[k].tiles_x;
+    return c * count;
+  };
+  while (!forced && ctas_of(P) < 2 * 148 && R - 4 >= r_min) {
+    R -= 4;
+    P = fused_geometry(p_, g_, R, tiles0);
+  }
+  while (!forced && ctas_of(P) < 148 && P.lv[0].tile_w > 128 && tiles0 < 8) {
     ++tiles0;
     P = fused_geometry(p_, g_, R, tiles0);
   }

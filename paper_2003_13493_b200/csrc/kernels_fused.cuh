@@ -85,6 +85,7 @@ struct Params {
   int nw_max;     // plane words per row, max over tiles
   int rp;         // score tile pitch (u16)
   int key_slots;  // shared cell-key capacity
+  int list_cap;   // corner-list capacity override (0 = default 6144 entries)
   uint32_t pow2[32];  // 1 << i, read from the constant bank so shifts can issue as IMAD
   uint32_t emask[8];  // ~0 where bit b of eps is set
   // In-cell key tables (DeviceBatch::keytab): per level, for every column x
@@ -102,7 +103,8 @@ struct Smem {
 // several rounds.
 __host__ __device__ inline int list_capacity(const Params& p) {
   const int worst = (p.R + 2 * p.radius) * p.nw_max * kOwn;
-  return worst < 6144 ? (worst + 7) & ~7 : 6144;
+  const int cap = p.list_cap > 0 ? p.list_cap : 6144;  // host override (tests force rounds)
+  return worst < cap ? (worst + 7) & ~7 : cap;
 }
 
 __host__ __device__ inline Smem smem_layout(const Params& p) {

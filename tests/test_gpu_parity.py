@@ -230,17 +230,22 @@ def test_unaligned_pitch_uses_plain_loads_and_matches(orc):
         assert (res[f] == ref).all()
 
 
+@pytest.mark.parametrize("cap", [0, 256, 1000])
 @pytest.mark.parametrize("kind", ["sad_b", "sad_a"])
-def test_dense_corners_multi_round_list(orc, kind):
-    """eps = 0 on noise makes most pixels corners, overflowing the shared
-    corner list: the kernel scores and suppresses in several rounds."""
+def test_dense_corners_multi_round_list(orc, kind, cap, monkeypatch):
+    """eps = 0 on noise makes ~40 % of pixels corners; with the corner list
+    capped (FLKB_LIST_CAP) every band overflows it and the kernel scores and
+    suppresses in several rounds. Results must not depend on the cap."""
+    if cap:
+        monkeypatch.setenv("FLKB_LIST_CAP", str(cap))
     img = synth.noise(77, 752, 480)
     cfg = dict(epsilon=0, N=9, score_kind=kind, l=2, w=1, h=16, n=1)
     feats, extra = fl.Detector(make_config(cfg)).run(img, stats=True)
     ref, st = orc.detect(img, oracle.make_params(**cfg))
     assert (feats == ref).all()
     assert extra["stats"]["nms_candidates"] == st.candidates
-    assert st.candidates > 200_000  # genuinely dense
+    assert extra["stats"]["nms_comparisons"] == st.comparisons
+    assert st.candidates > 150_000  # genuinely dense
 
 
 @pytest.mark.parametrize("n", [2, 3, 4])
