@@ -325,14 +325,7 @@ void DeviceBatch::run(const uint8_t* frames, size_t fstride, int pitch, int coun
     P.lv[k].kt_row = kt_row_[k];
   }
   P.stats = stats ? st : nullptr;
-  P.ctas_per_frame = ctas;
-  P.items = ctas * count;
-  P.div_cpf = fused::FastDiv::make(static_cast<uint32_t>(ctas));
-  if (sms_ == 0) check_cuda(cudaDeviceGetAttribute(&sms_, cudaDevAttrMultiProcessorCount, device_),
-                            "SM count");
-  // persistent grid: every resident CTA slot, each walking items with stride G
-  const int grid = std::min(P.items, sms_ * fused::kMinBlocks);
-  kern<<<grid, fused::kThreads, smem, s>>>(P);
+  kern<<<dim3(ctas, count), fused::kThreads, smem, s>>>(P);
   ++launched;
   if (times) check_cuda(cudaEventRecord(ev[2], s), "cudaEventRecord");
   k_compact<<<count, 256, 0, s>>>(keys, g_.cols, g_.cells, feats, counts);

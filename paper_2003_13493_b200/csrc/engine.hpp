@@ -115,7 +115,6 @@ class DeviceBatch {
   uint64_t* d_stats_ = nullptr;  // [capacity][2] = candidates, comparisons
   float* d_naive_ = nullptr;     // conformance scratch (lazily allocated)
   uint32_t* d_keytab_ = nullptr; // in-cell key tables of the fused kernel, per level
-  int sms_ = 0;                  // SM count of the device (persistent grid size)
   int kt_col_[kMaxLevels] = {}, kt_row_[kMaxLevels] = {};
   size_t fused_smem_ = 0;        // dynamic shared memory of the fused kernel
   int fused_R_ = 32;             // rows per band (largest that fits kMinBlocks CTAs/SM)

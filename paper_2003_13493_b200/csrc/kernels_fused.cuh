@@ -86,8 +86,6 @@ struct Params {
   int rp;         // score tile pitch (u16)
   int key_slots;  // shared cell-key capacity
   int list_cap;   // corner-list capacity override (0 = default 6144 entries)
-  int ctas_per_frame, items;  // work items: frames x (bands x tiles over all levels)
-  FastDiv div_cpf;
   uint32_t pow2[32];  // 1 << i, read from the constant bank so shifts can issue as IMAD
   uint32_t emask[8];  // ~0 where bit b of eps is set
   // In-cell key tables (DeviceBatch::keytab): per level, for every column x
@@ -298,68 +296,29 @@ struct TaskIter {
   }
 };
 
-// One work item: (frame, level, band of R rows, column tile) and the staging
-// geometry of its rows.
-struct Item {
-  int f, k, y0, y1, x_lo, x_hi, iy0, ya, yb, bx0, gx0, sx0, row_bytes;
-};
-
-__device__ __forceinline__ Item decode_item(const Params& P, int item, int n) {
-  Item it;
-  it.f = P.div_cpf(item);
-  const int c = item - it.f * P.ctas_per_frame;
-  int k = 0;
-  while (k + 1 < P.levels && c >= P.lv[k + 1].cta0) ++k;
-  const Level& L = P.lv[k];
-  const int local = c - L.cta0;
-  const int band = L.div_tiles(local), tile = local - band * L.tiles_x;
-  it.k = k;
-  it.y0 = band * P.R;
-  it.y1 = min(it.y0 + P.R, L.h);
-  it.x_lo = tile * L.tile_w;
-  it.x_hi = min(it.x_lo + L.tile_w, L.w);
-  it.iy0 = it.y0 - n - 3;  // stage row 0 <-> image row iy0
-  it.ya = max(it.iy0, 0);  // rows present in the stage: [ya, yb)
-  it.yb = min(it.y1 + n + 3, L.h);
-  it.bx0 = (it.x_lo - n - 3) & ~15;  // stage column 0 <-> image x bx0
-  it.gx0 = max(it.bx0, 0);
-  it.sx0 = it.gx0 - it.bx0;  // multiple of 16
-  int rb = min(it.bx0 + P.sw, L.pitch) - it.gx0;
-  rb = min(rb, ((L.w + 15) & ~15) - it.gx0);
-  it.row_bytes = L.tma ? (rb & ~15) : rb;
-  return it;
-}
-
-// One elected thread: cp.async.bulk every staged row of `it` into shared
-// memory, completing on the mbarrier.
-__device__ __forceinline__ void issue_stage(const Params& P, const Item& it, uint8_t* stage,
-                                            uint32_t bar_s) {
-  const Level& L = P.lv[it.k];
-  const uint8_t* frame = L.img + it.f * L.fstride;
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-  const uint32_t bytes = static_cast<uint32_t>(it.row_bytes * (it.yb - it.ya));
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar_s), "r"(bytes)
-               : "memory");
-  for (int y = it.ya; y < it.yb; ++y) {
-    const uint32_t dst = static_cast<uint32_t>(
-        __cvta_generic_to_shared(stage + (y - it.iy0) * P.sw + it.sx0));
-    const uint8_t* src = frame + static_cast<size_t>(y) * L.pitch + it.gx0;
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
-            "r"(dst), "l"(src), "r"(it.row_bytes), "r"(bar_s)
-        : "memory");
-  }
-}
-
-// Persistent: CTA c processes items c, c + G, c + 2G, ... (G = gridDim.x).
-// Item i+1's rows are fetched by TMA while item i is in its suppression
-// phase (its stage is dead by then), so the copy latency hides behind work.
 template <int N, int KIND, int RADIUS>
 __global__ void __launch_bounds__(kThreads, kMinBlocks) k_detect(const __grid_constant__ Params P) {
   extern __shared__ __align__(128) uint8_t smem[];
   const Smem S = smem_layout(P);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int n = RADIUS > 0 ? RADIUS : P.radius;
+
+  // --- which level, band and column tile
+  int k = 0;
+  while (k + 1 < P.levels && static_cast<int>(blockIdx.x) >= P.lv[k + 1].cta0) ++k;
+  const Level& L = P.lv[k];
+  const int local = blockIdx.x - L.cta0;
+  const int band = L.div_tiles(local), tile = local - band * L.tiles_x;
+  const int f = blockIdx.y;
+  const int n = RADIUS > 0 ? RADIUS : P.radius, w = L.w, h = L.h;
+  const int y0 = band * P.R, y1 = min(y0 + P.R, h);          // rows suppressed here
+  const int x_lo = tile * L.tile_w, x_hi = min(x_lo + L.tile_w, w);
+  const int fy0 = y0 - n;                                       // tile row 0 <-> image row fy0
+  const int iy0 = fy0 - 3;                                      // stage row 0 <-> image row iy0
+  const int ya = max(iy0, 0), yb = min(y1 + n + 3, h);          // rows present in the stage
+  const int bx0 = (x_lo - n - 3) & ~15;                         // stage column 0 <-> image x bx0
+  const int nw = L.nw;                                          // plane words per row
+  const int cx_lo = max(x_lo - n, 3), cx_hi = min(x_hi + n, w - 3);  // FAST columns
+  const int cy_lo = max(fy0, 3), cy_hi = min(y1 + n, h - 3);         // FAST rows
 
   uint8_t* stage = smem + S.stage;
   uint32_t* planes = reinterpret_cast<uint32_t*>(smem + S.planes);
@@ -371,401 +330,391 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_detect(const __grid_co
   // so a warp's 16-byte accesses to consecutive words are bank-conflict free
   const int half = (P.R + 2 * n + 6) * P.nw_max * 4;
   uint32_t* skeys = reinterpret_cast<uint32_t*>(smem + S.skeys);
-  const uint32_t bar_s =
-      static_cast<uint32_t>(__cvta_generic_to_shared(reinterpret_cast<uint64_t*>(smem + S.bar)));
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + S.bar);
 
-  int item = blockIdx.x;
-  if (item >= P.items) return;
-  if (tid == 0) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar_s));
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  Item it = decode_item(P, item, n);
-  if (tid == 0 && P.lv[it.k].tma) issue_stage(P, it, stage, bar_s);
-  uint32_t parity = 0;
+  // cell rows touched by the suppressed rows [y0, y1) of level k
+  const int cr0 = P.div_ch(y0 << k);
+  const int cr1 = y1 > y0 ? P.div_ch((y1 - 1) << k) : cr0;
+  const int slots = (cr1 - cr0 + 1) * P.cols;
+  const bool local_keys = slots <= P.key_slots;
 
-  for (;;) {
-    const Level& L = P.lv[it.k];
-    const int k = it.k, f = it.f, w = L.w, h = L.h;
-    const int y0 = it.y0, y1 = it.y1, x_lo = it.x_lo, x_hi = it.x_hi;
-    const int fy0 = y0 - n, iy0 = it.iy0, ya = it.ya, yb = it.yb, bx0 = it.bx0;
-    const int nw = L.nw;
-    const int cx_lo = max(x_lo - n, 3), cx_hi = min(x_hi + n, w - 3);  // FAST columns
-    const int cy_lo = max(fy0, 3), cy_hi = min(y1 + n, h - 3);         // FAST rows
-    // cell rows touched by the suppressed rows [y0, y1) of level k
-    const int cr0 = P.div_ch(y0 << k);
-    const int cr1 = y1 > y0 ? P.div_ch((y1 - 1) << k) : cr0;
-    const int slots = (cr1 - cr0 + 1) * P.cols;
-    const bool local_keys = slots <= P.key_slots;
-
-    // --- 1. stage rows [ya, yb) (TMA: issued earlier; plain loads otherwise)
-    if (!L.tma) {
-      const uint8_t* frame = L.img + f * L.fstride;
-      for (int i = tid; i < (yb - ya) * it.row_bytes; i += kThreads) {
-        const int y = ya + i / it.row_bytes, x = i % it.row_bytes;
-        stage[(y - iy0) * P.sw + it.sx0 + x] =
-            frame[static_cast<size_t>(y) * L.pitch + it.gx0 + x];
-      }
-    }
-    if (local_keys)
-      for (int i = tid; i < slots; i += kThreads) skeys[i] = 0u;
-    __syncthreads();
-    if (L.tma) {
-      uint32_t done = 0;
-      while (!done) {
+  // --- 1. stage the rows [ya, yb), columns [max(bx0,0), ...) of this tile
+  const uint8_t* frame = L.img + f * L.fstride;
+  const int gx0 = max(bx0, 0);
+  const int sx0 = gx0 - bx0;  // multiple of 16
+  int row_bytes = min(bx0 + P.sw, L.pitch) - gx0;
+  row_bytes = min(row_bytes, ((w + 15) & ~15) - gx0);
+  if (L.tma) {
+    row_bytes &= ~15;
+    if (tid == 0) {
+      const uint32_t b = static_cast<uint32_t>(__cvta_generic_to_shared(bar));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(b));
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      const uint32_t bytes = static_cast<uint32_t>(row_bytes * (yb - ya));
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(bytes)
+                   : "memory");
+      for (int y = ya; y < yb; ++y) {
+        const uint32_t dst = static_cast<uint32_t>(
+            __cvta_generic_to_shared(stage + (y - iy0) * P.sw + sx0));
+        const uint8_t* src = frame + static_cast<size_t>(y) * L.pitch + gx0;
         asm volatile(
-            "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
-            : "=r"(done)
-            : "r"(bar_s), "r"(parity)
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+                "r"(dst), "l"(src), "r"(row_bytes), "r"(b)
             : "memory");
       }
-      parity ^= 1u;
     }
+  } else {
+    for (int i = tid; i < (yb - ya) * row_bytes; i += kThreads) {
+      const int y = ya + i / row_bytes, x = i % row_bytes;
+      stage[(y - iy0) * P.sw + sx0 + x] = frame[static_cast<size_t>(y) * L.pitch + gx0 + x];
+    }
+  }
+  if (local_keys)
+    for (int i = tid; i < slots; i += kThreads) skeys[i] = 0u;
+  __syncthreads();
+  if (L.tma) {
+    const uint32_t b = static_cast<uint32_t>(__cvta_generic_to_shared(bar));
+    uint32_t done = 0;
+    while (!done) {
+      asm volatile(
+          "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0; selp.u32 %0, 1, 0, p; }"
+          : "=r"(done)
+          : "r"(b)
+          : "memory");
+    }
+  }
 
-    // --- 2. bit planes of every staged row
-    {
-      const int tasks = (yb - ya) * nw;
-      TaskIter it(tid, nw, L.div_nw);
-      for (int t = tid; t < tasks; t += kThreads, it.next()) {
-        const int r = ya - iy0 + it.row, j = it.j;
-        const int bx = kOwn * j;
-        const uint32_t* src = reinterpret_cast<const uint32_t*>(stage + r * P.sw + (bx & ~3));
-        uint32_t a[9], wv[8], pl[8];
-  #pragma unroll
-        for (int i = 0; i < 9; ++i) a[i] = src[i];
-        const uint32_t sel = (bx & 2) ? 0x5432u : 0x3210u;
-  #pragma unroll
-        for (int i = 0; i < 8; ++i) wv[i] = __byte_perm(a[i], a[i + 1], sel);
-        transpose32x8(wv, pl, P.pow2);
-        uint32_t* dst = planes + (r * P.nw_max + j) * 4;
-        *reinterpret_cast<uint4*>(dst) = make_uint4(pl[0], pl[1], pl[2], pl[3]);
-        *reinterpret_cast<uint4*>(dst + half) = make_uint4(pl[4], pl[5], pl[6], pl[7]);
-      }
+  // --- 2. bit planes of every staged row
+  {
+    const int tasks = (yb - ya) * nw;
+    TaskIter it(tid, nw, L.div_nw);
+    for (int t = tid; t < tasks; t += kThreads, it.next()) {
+      const int r = ya - iy0 + it.row, j = it.j;
+      const int bx = kOwn * j;
+      const uint32_t* src = reinterpret_cast<const uint32_t*>(stage + r * P.sw + (bx & ~3));
+      uint32_t a[9], wv[8], pl[8];
+#pragma unroll
+      for (int i = 0; i < 9; ++i) a[i] = src[i];
+      const uint32_t sel = (bx & 2) ? 0x5432u : 0x3210u;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) wv[i] = __byte_perm(a[i], a[i + 1], sel);
+      transpose32x8(wv, pl, P.pow2);
+      uint32_t* dst = planes + (r * P.nw_max + j) * 4;
+      *reinterpret_cast<uint4*>(dst) = make_uint4(pl[0], pl[1], pl[2], pl[3]);
+      *reinterpret_cast<uint4*>(dst + half) = make_uint4(pl[4], pl[5], pl[6], pl[7]);
     }
-    __syncthreads();
-  
-    // --- 3. bit-sliced corner masks for the FAST rows
-    const int fast_rows = cy_hi - cy_lo;
-    {
-      const uint32_t (&E)[8] = P.emask;  // eps bit masks, constant-bank operands
-      const int tasks = max(fast_rows, 0) * nw;
-      TaskIter it(tid, nw, L.div_nw);
-      for (int t = tid; t < tasks; t += kThreads, it.next()) {
-        const int y = cy_lo + it.row, j = it.j;
-        const int r = y - iy0;  // stage/plane row of the centre
-        const uint32_t* base = planes + j * 4;
-        auto row_planes = [&](int rr, uint32_t (&q)[8]) {
-          const uint32_t* q4 = base + rr * P.nw_max * 4;
-          const uint4 u = *reinterpret_cast<const uint4*>(q4);
-          const uint4 v = *reinterpret_cast<const uint4*>(q4 + half);
-          q[0] = u.x; q[1] = u.y; q[2] = u.z; q[3] = u.w;
-          q[4] = v.x; q[5] = v.y; q[6] = v.z; q[7] = v.w;
-        };
-        uint32_t c[8], lo[8], hi[8];
-        row_planes(r, c);
-        {
-          uint32_t br = 0, cy = 0;
-  #pragma unroll
-          for (int b = 0; b < 8; ++b) {
-            // plain C so ptxas can take E[b] straight from the constant bank
-            lo[b] = c[b] ^ E[b] ^ br;
-            br = (~c[b] & E[b]) | (~c[b] & br) | (E[b] & br);
-            hi[b] = c[b] ^ E[b] ^ cy;
-            cy = (c[b] & E[b]) | (c[b] & cy) | (E[b] & cy);
-          }
-  #pragma unroll
-          for (int b = 0; b < 8; ++b) {
-            lo[b] &= ~br;  // c - eps < 0  -> 0
-            hi[b] |= cy;   // c + eps > 255 -> 255
-          }
+  }
+  __syncthreads();
+
+  // --- 3. bit-sliced corner masks for the FAST rows
+  const int fast_rows = cy_hi - cy_lo;
+  {
+    const uint32_t (&E)[8] = P.emask;  // eps bit masks, constant-bank operands
+    const int tasks = max(fast_rows, 0) * nw;
+    TaskIter it(tid, nw, L.div_nw);
+    for (int t = tid; t < tasks; t += kThreads, it.next()) {
+      const int y = cy_lo + it.row, j = it.j;
+      const int r = y - iy0;  // stage/plane row of the centre
+      const uint32_t* base = planes + j * 4;
+      auto row_planes = [&](int rr, uint32_t (&q)[8]) {
+        const uint32_t* q4 = base + rr * P.nw_max * 4;
+        const uint4 u = *reinterpret_cast<const uint4*>(q4);
+        const uint4 v = *reinterpret_cast<const uint4*>(q4 + half);
+        q[0] = u.x; q[1] = u.y; q[2] = u.z; q[3] = u.w;
+        q[4] = v.x; q[5] = v.y; q[6] = v.z; q[7] = v.w;
+      };
+      uint32_t c[8], lo[8], hi[8];
+      row_planes(r, c);
+      {
+        uint32_t br = 0, cy = 0;
+#pragma unroll
+        for (int b = 0; b < 8; ++b) {
+          // plain C so ptxas can take E[b] straight from the constant bank
+          lo[b] = c[b] ^ E[b] ^ br;
+          br = (~c[b] & E[b]) | (~c[b] & br) | (E[b] & br);
+          hi[b] = c[b] ^ E[b] ^ cy;
+          cy = (c[b] & E[b]) | (c[b] & cy) | (E[b] & cy);
         }
-        uint32_t dk[16], bk[16];
-  #pragma unroll
-        for (int dy = -3; dy <= 3; ++dy) {
-          uint32_t q[8];
-          row_planes(r + dy, q);
-  #pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            if (ring_dy(i) != dy) continue;
-            const int dx = ring_dx(i);
-            uint32_t s[8];
-  #pragma unroll
-            for (int b = 0; b < 8; ++b) s[b] = shift_fma(q[b], dx, P.pow2);
-            dk[i] = sliced_less(s, lo);
-            bk[i] = sliced_less(hi, s);
-          }
+#pragma unroll
+        for (int b = 0; b < 8; ++b) {
+          lo[b] &= ~br;  // c - eps < 0  -> 0
+          hi[b] |= cy;   // c + eps > 255 -> 255
         }
-        uint32_t corner = sliced_arc<N>(dk) | sliced_arc<N>(bk);
-        // owned bits [3, 29) that fall inside the FAST columns
-        const int xb = bx0 + kOwn * j;
-        const int lo_b = max(3, cx_lo - xb), hi_b = min(29, cx_hi - xb);
-        const uint32_t valid = hi_b > lo_b ? ((hi_b >= 32 ? 0xFFFFFFFFu : ((1u << hi_b) - 1u)) &
-                                              ~((1u << lo_b) - 1u))
-                                           : 0u;
-        cm[t] = corner & valid;
       }
+      uint32_t dk[16], bk[16];
+#pragma unroll
+      for (int dy = -3; dy <= 3; ++dy) {
+        uint32_t q[8];
+        row_planes(r + dy, q);
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          if (ring_dy(i) != dy) continue;
+          const int dx = ring_dx(i);
+          uint32_t s[8];
+#pragma unroll
+          for (int b = 0; b < 8; ++b) s[b] = shift_fma(q[b], dx, P.pow2);
+          dk[i] = sliced_less(s, lo);
+          bk[i] = sliced_less(hi, s);
+        }
+      }
+      uint32_t corner = sliced_arc<N>(dk) | sliced_arc<N>(bk);
+      // owned bits [3, 29) that fall inside the FAST columns
+      const int xb = bx0 + kOwn * j;
+      const int lo_b = max(3, cx_lo - xb), hi_b = min(29, cx_hi - xb);
+      const uint32_t valid = hi_b > lo_b ? ((hi_b >= 32 ? 0xFFFFFFFFu : ((1u << hi_b) - 1u)) &
+                                            ~((1u << lo_b) - 1u))
+                                         : 0u;
+      cm[t] = corner & valid;
     }
-    __syncthreads();
-  
-    // --- 4. one CTA-wide corner list (row-major task order) from a block scan
-    //        of per-task corner counts; the score tile (aliasing the dead
-    //        planes) is zeroed meanwhile. Entries: (row - cy_lo) << 10 | stage column.
-    const int tasks_f = max(fast_rows, 0) * nw;
-    const int per = (tasks_f + kThreads - 1) / kThreads;
-    const int tb = min(tid * per, tasks_f), te = min(tb + per, tasks_f);
-    int cnt = 0;
-    for (int t = tb; t < te; ++t) cnt += __popc(cm[t]);
-    {
-      uint4* z = reinterpret_cast<uint4*>(tile_s);
-      const int n16 = ((P.R + 2 * n) * P.rp * 2) / 16;
-      for (int i = tid; i < n16; i += kThreads) z[i] = make_uint4(0, 0, 0, 0);
-    }
-    int incl = cnt;
-  #pragma unroll
+  }
+  __syncthreads();
+
+  // --- 4. one CTA-wide corner list (row-major task order) from a block scan
+  //        of per-task corner counts; the score tile (aliasing the dead
+  //        planes) is zeroed meanwhile. Entries: (row - cy_lo) << 10 | stage column.
+  const int tasks_f = max(fast_rows, 0) * nw;
+  const int per = (tasks_f + kThreads - 1) / kThreads;
+  const int tb = min(tid * per, tasks_f), te = min(tb + per, tasks_f);
+  int cnt = 0;
+  for (int t = tb; t < te; ++t) cnt += __popc(cm[t]);
+  {
+    uint4* z = reinterpret_cast<uint4*>(tile_s);
+    const int n16 = ((P.R + 2 * n) * P.rp * 2) / 16;
+    for (int i = tid; i < n16; i += kThreads) z[i] = make_uint4(0, 0, 0, 0);
+  }
+  int incl = cnt;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int v = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += v;
+  }
+  if (lane == 31) scan[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    const int v = lane < kWarps ? scan[lane] : 0;
+    int acc = v;
+#pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-      const int v = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += v;
+      const int u = __shfl_up_sync(0xffffffffu, acc, o);
+      if (lane >= o) acc += u;
     }
-    if (lane == 31) scan[warp] = incl;
-    __syncthreads();
-    if (warp == 0) {
-      const int v = lane < kWarps ? scan[lane] : 0;
-      int acc = v;
-  #pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int u = __shfl_up_sync(0xffffffffu, acc, o);
-        if (lane >= o) acc += u;
-      }
-      if (lane < kWarps) scan[lane] = acc - v;
-      if (lane == 31) scan[kWarps] = scan[kWarps + 1] = scan[kWarps + 2] = acc;
+    if (lane < kWarps) scan[lane] = acc - v;
+    if (lane == 31) scan[kWarps] = scan[kWarps + 1] = scan[kWarps + 2] = acc;
+  }
+  __syncthreads();
+  const int base = scan[warp] + incl - cnt;  // this thread's first list index
+  const int total = scan[kWarps];
+  // List range of the suppressed rows [y0, y1): tasks [T0, T1) are row-major,
+  // so their corners are entries [e_lo, e_hi); the owner of task T records
+  // its list index (read after the scoring barrier).
+  const int T0 = min(max(max(y0, 3) - cy_lo, 0) * nw, tasks_f);
+  const int T1 = min(max(min(y1, h - 3) - cy_lo, 0) * nw, tasks_f);
+  if (tb < te) {
+    int pos = base;
+    for (int t = tb; t < te; ++t) {
+      if (t == T0) scan[kWarps + 1] = pos;
+      if (t == T1) scan[kWarps + 2] = pos;
+      pos += __popc(cm[t]);
     }
-    __syncthreads();
-    const int base = scan[warp] + incl - cnt;  // this thread's first list index
-    const int total = scan[kWarps];
-    // List range of the suppressed rows [y0, y1): tasks [T0, T1) are row-major,
-    // so their corners are entries [e_lo, e_hi); the owner of task T records
-    // its list index (read after the scoring barrier).
-    const int T0 = min(max(max(y0, 3) - cy_lo, 0) * nw, tasks_f);
-    const int T1 = min(max(min(y1, h - 3) - cy_lo, 0) * nw, tasks_f);
-    if (tb < te) {
-      int pos = base;
-      for (int t = tb; t < te; ++t) {
-        if (t == T0) scan[kWarps + 1] = pos;
-        if (t == T1) scan[kWarps + 2] = pos;
-        pos += __popc(cm[t]);
-      }
-    }
-    const int cap = list_capacity(P);
-    const int row_tb = L.div_nw(tb), j_tb = tb - row_tb * nw;
-    // Writes the entries with list index in [w0, w0 + cap) to list[index - w0].
-    auto build = [&](int w0) {
-      if (total <= cap) {
-        // Common case, every entry fits: per word slot, the warp either lets each
-        // lane walk its own bits (cost ~ max popc) or expands the non-empty words
-        // one at a time across the lanes (cost ~ non-empty words), whichever is
-        // cheaper for this slot.
-        int pos = base, row = row_tb, j = j_tb;
-        for (int q = 0; q < per; ++q) {
-          const int t = tb + q;
-          uint32_t m = t < te ? cm[t] : 0u;
-          const uint32_t e0 = (static_cast<uint32_t>(row) << 10) | static_cast<uint32_t>(kOwn * j);
-          const int c = __popc(m);
-          const unsigned nz = __ballot_sync(0xffffffffu, m != 0u);
-          const int mx = __reduce_max_sync(0xffffffffu, c);
-          if (2 * mx <= 3 * __popc(nz)) {
-            int p = pos;
-            while (m) {
-              const int b = __ffs(m) - 1;
-              m &= m - 1;
-              list[p++] = static_cast<uint16_t>(e0 + b);
-            }
-          } else {
-            unsigned z = nz;
-            while (z) {
-              const int src = __ffs(z) - 1;
-              z &= z - 1;
-              const uint32_t wv = __shfl_sync(0xffffffffu, m, src);
-              const int p = __shfl_sync(0xffffffffu, pos, src);
-              const uint32_t e = __shfl_sync(0xffffffffu, e0, src);
-              if ((wv >> lane) & 1u)
-                list[p + __popc(wv & ((1u << lane) - 1u))] = static_cast<uint16_t>(e + lane);
-            }
-          }
-          pos += c;
-          if (++j == nw) {
-            j = 0;
-            ++row;
-          }
-        }
-        return;
-      }
-      if (base >= w0 + cap || base + cnt <= w0) return;
+  }
+  const int cap = list_capacity(P);
+  const int row_tb = L.div_nw(tb), j_tb = tb - row_tb * nw;
+  // Writes the entries with list index in [w0, w0 + cap) to list[index - w0].
+  auto build = [&](int w0) {
+    if (total <= cap) {
+      // Common case, every entry fits: per word slot, the warp either lets each
+      // lane walk its own bits (cost ~ max popc) or expands the non-empty words
+      // one at a time across the lanes (cost ~ non-empty words), whichever is
+      // cheaper for this slot.
       int pos = base, row = row_tb, j = j_tb;
-      for (int t = tb; t < te; ++t) {
-        uint32_t m = cm[t];
+      for (int q = 0; q < per; ++q) {
+        const int t = tb + q;
+        uint32_t m = t < te ? cm[t] : 0u;
         const uint32_t e0 = (static_cast<uint32_t>(row) << 10) | static_cast<uint32_t>(kOwn * j);
-        while (m) {
-          const int b = __ffs(m) - 1;
-          m &= m - 1;
-          if (pos >= w0 && pos < w0 + cap) list[pos - w0] = static_cast<uint16_t>(e0 + b);
-          ++pos;
+        const int c = __popc(m);
+        const unsigned nz = __ballot_sync(0xffffffffu, m != 0u);
+        const int mx = __reduce_max_sync(0xffffffffu, c);
+        if (2 * mx <= 3 * __popc(nz)) {
+          int p = pos;
+          while (m) {
+            const int b = __ffs(m) - 1;
+            m &= m - 1;
+            list[p++] = static_cast<uint16_t>(e0 + b);
+          }
+        } else {
+          unsigned z = nz;
+          while (z) {
+            const int src = __ffs(z) - 1;
+            z &= z - 1;
+            const uint32_t wv = __shfl_sync(0xffffffffu, m, src);
+            const int p = __shfl_sync(0xffffffffu, pos, src);
+            const uint32_t e = __shfl_sync(0xffffffffu, e0, src);
+            if ((wv >> lane) & 1u)
+              list[p + __popc(wv & ((1u << lane) - 1u))] = static_cast<uint16_t>(e + lane);
+          }
         }
+        pos += c;
         if (++j == nw) {
           j = 0;
           ++row;
         }
       }
-    };
-    // Score-tile column of stage column xs: xs + bx0 - (x_lo - 2n), i.e. an n-wide
-    // zero margin left of the FAST columns.
-    const int tcol = bx0 - (x_lo - 2 * n);
-    for (int w0 = 0; w0 < total; w0 += cap) {
-      if (w0 > 0) __syncthreads();  // the previous round's entries are consumed
-      build(w0);
-      __syncthreads();
-      const int m_end = min(cap, total - w0);
-      for (int e = tid; e < m_end; e += kThreads) {
-        const int ent = list[e];
-        const int y = cy_lo + (ent >> 10), xs = ent & 1023;
-        const uint8_t* sp = stage + (y - iy0) * P.sw + xs;
-        const uint32_t cc = sp[0];
-        int sc;
-        if (KIND == kSadB) {
-          uint32_t rb[16];
-  #pragma unroll
-          for (int i = 0; i < 16; ++i) rb[i] = sp[ring_dy(i) * P.sw + ring_dx(i)];
-          uint32_t pk[4];
-  #pragma unroll
-          for (int q = 0; q < 4; ++q)
-            pk[q] = __byte_perm(__byte_perm(rb[4 * q], rb[4 * q + 1], 0x0040),
-                                __byte_perm(rb[4 * q + 2], rb[4 * q + 3], 0x0040), 0x5410);
-          sc = sad_b_packed(pk, cc, static_cast<uint32_t>(P.eps));
-        } else {
-          int ring[16];
-  #pragma unroll
-          for (int i = 0; i < 16; ++i) ring[i] = sp[ring_dy(i) * P.sw + ring_dx(i)];
-          sc = fast_score<N, KIND>(static_cast<int>(cc), ring, P.eps);
-        }
-        tile_s[(y - fy0) * P.rp + xs + tcol] = static_cast<uint16_t>(sc);
+      return;
+    }
+    if (base >= w0 + cap || base + cnt <= w0) return;
+    int pos = base, row = row_tb, j = j_tb;
+    for (int t = tb; t < te; ++t) {
+      uint32_t m = cm[t];
+      const uint32_t e0 = (static_cast<uint32_t>(row) << 10) | static_cast<uint32_t>(kOwn * j);
+      while (m) {
+        const int b = __ffs(m) - 1;
+        m &= m - 1;
+        if (pos >= w0 && pos < w0 + cap) list[pos - w0] = static_cast<uint16_t>(e0 + b);
+        ++pos;
+      }
+      if (++j == nw) {
+        j = 0;
+        ++row;
       }
     }
+  };
+  // Score-tile column of stage column xs: xs + bx0 - (x_lo - 2n), i.e. an n-wide
+  // zero margin left of the FAST columns.
+  const int tcol = bx0 - (x_lo - 2 * n);
+  for (int w0 = 0; w0 < total; w0 += cap) {
+    if (w0 > 0) __syncthreads();  // the previous round's entries are consumed
+    build(w0);
     __syncthreads();
-
-    // the stage is dead: prefetch the next item's rows behind this item's NMS
-    const int nxt = item + static_cast<int>(gridDim.x);
-    const bool has_next = nxt < P.items;
-    Item nx = it;
-    if (has_next) {
-      nx = decode_item(P, nxt, n);
-      if (tid == 0 && P.lv[nx.k].tma) issue_stage(P, nx, stage, bar_s);
+    const int m_end = min(cap, total - w0);
+    for (int e = tid; e < m_end; e += kThreads) {
+      const int ent = list[e];
+      const int y = cy_lo + (ent >> 10), xs = ent & 1023;
+      const uint8_t* sp = stage + (y - iy0) * P.sw + xs;
+      const uint32_t cc = sp[0];
+      int sc;
+      if (KIND == kSadB) {
+        uint32_t rb[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) rb[i] = sp[ring_dy(i) * P.sw + ring_dx(i)];
+        uint32_t pk[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          pk[q] = __byte_perm(__byte_perm(rb[4 * q], rb[4 * q + 1], 0x0040),
+                              __byte_perm(rb[4 * q + 2], rb[4 * q + 3], 0x0040), 0x5410);
+        sc = sad_b_packed(pk, cc, static_cast<uint32_t>(P.eps));
+      } else {
+        int ring[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) ring[i] = sp[ring_dy(i) * P.sw + ring_dx(i)];
+        sc = fast_score<N, KIND>(static_cast<int>(cc), ring, P.eps);
+      }
+      tile_s[(y - fy0) * P.rp + xs + tcol] = static_cast<uint16_t>(sc);
     }
+  }
+  __syncthreads();
 
-    // --- 5. suppression + per-cell keys for the candidates in rows [y0, y1):
-    //        a contiguous range of the list, since tasks are row-major
-    unsigned long long n_cand = 0, n_cmp = 0;
-    {
-      const int nx_lo = max(x_lo, 3), nx_hi = min(x_hi, w - 3);
-      const int e_lo = T1 > T0 ? scan[kWarps + 1] : 0;
-      const int e_hi = T1 > T0 ? scan[kWarps + 2] : 0;
-      const int rp = P.rp;
-      for (int w0 = e_lo; w0 < e_hi; w0 += cap) {
-        const bool resident = total <= cap;  // the scoring list is still in place
-        const int off = resident ? 0 : w0;
-        if (!resident) {
-          __syncthreads();
-          build(w0);
-          __syncthreads();
-        }
-        const int m_end = resident ? e_hi : min(w0 + cap, e_hi);
-        for (int e = w0 + tid; e < m_end; e += kThreads) {
-          const int ent = list[e - off];
-          const int y = cy_lo + (ent >> 10), xs = ent & 1023;
-          const int x = bx0 + xs;
-          if (x < nx_lo || x >= nx_hi) continue;  // halo column of a neighbouring tile
-          const uint16_t* row = tile_s + (y - fy0) * rp + xs + tcol;
-          const int s = row[0];
-          if (s == 0) continue;  // a corner whose score is 0 (MT, eps 0) is no candidate
-          bool keep = true;
-          if (P.stats) {
-            ++n_cand;
-            uint32_t cmp = 0;
-            for (int rr = 1; rr <= n && keep; ++rr) {
-              auto visit = [&](int dx, int dy) {
-                if (!keep) return;
-                const int nx = x + dx, ny = y + dy;
-                if (nx < 0 || ny < 0 || nx >= w || ny >= h) return;
-                ++cmp;
-                const int v = row[dy * rp + dx];
-                if (v > s || (v == s && (dy < 0 || (dy == 0 && dx < 0)))) keep = false;
-              };
-              for (int dx = -rr; dx <= rr; ++dx) visit(dx, -rr);
-              for (int dy = -rr + 1; dy <= rr; ++dy) visit(rr, dy);
-              for (int dx = rr - 1; dx >= -rr; --dx) visit(dx, rr);
-              for (int dy = rr - 1; dy >= -rr + 1; --dy) visit(-rr, dy);
-            }
-            n_cmp += cmp;
-          } else if (RADIUS == 1) {
-            // earlier neighbours must be strictly lower, later ones not higher;
-            // out-of-image neighbours read the tile's zero margin
-            const int e0 = max(max(row[-rp - 1], row[-rp]), max(row[-rp + 1], row[-1]));
-            const int l0 = max(max(row[1], row[rp - 1]), max(row[rp], row[rp + 1]));
-            keep = e0 < s && l0 <= s;
-          } else {
-            for (int dy = -n; dy <= n && keep; ++dy)
-              for (int dx = -n; dx <= n; ++dx) {
-                const int v = row[dy * rp + dx];
-                const bool earlier = dy < 0 || (dy == 0 && dx < 0);
-                if (v > s || (v == s && earlier)) {
-                  keep = false;
-                  break;
-                }
+  // --- 5. suppression + per-cell keys for the candidates in rows [y0, y1):
+  //        a contiguous range of the list, since tasks are row-major
+  unsigned long long n_cand = 0, n_cmp = 0;
+  {
+    const int nx_lo = max(x_lo, 3), nx_hi = min(x_hi, w - 3);
+    const int e_lo = T1 > T0 ? scan[kWarps + 1] : 0;
+    const int e_hi = T1 > T0 ? scan[kWarps + 2] : 0;
+    const int rp = P.rp;
+    for (int w0 = e_lo; w0 < e_hi; w0 += cap) {
+      const bool resident = total <= cap;  // the scoring list is still in place
+      const int off = resident ? 0 : w0;
+      if (!resident) {
+        __syncthreads();
+        build(w0);
+        __syncthreads();
+      }
+      const int m_end = resident ? e_hi : min(w0 + cap, e_hi);
+      for (int e = w0 + tid; e < m_end; e += kThreads) {
+        const int ent = list[e - off];
+        const int y = cy_lo + (ent >> 10), xs = ent & 1023;
+        const int x = bx0 + xs;
+        if (x < nx_lo || x >= nx_hi) continue;  // halo column of a neighbouring tile
+        const uint16_t* row = tile_s + (y - fy0) * rp + xs + tcol;
+        const int s = row[0];
+        if (s == 0) continue;  // a corner whose score is 0 (MT, eps 0) is no candidate
+        bool keep = true;
+        if (P.stats) {
+          ++n_cand;
+          uint32_t cmp = 0;
+          for (int rr = 1; rr <= n && keep; ++rr) {
+            auto visit = [&](int dx, int dy) {
+              if (!keep) return;
+              const int nx = x + dx, ny = y + dy;
+              if (nx < 0 || ny < 0 || nx >= w || ny >= h) return;
+              ++cmp;
+              const int v = row[dy * rp + dx];
+              if (v > s || (v == s && (dy < 0 || (dy == 0 && dx < 0)))) keep = false;
+            };
+            for (int dx = -rr; dx <= rr; ++dx) visit(dx, -rr);
+            for (int dy = -rr + 1; dy <= rr; ++dy) visit(rr, dy);
+            for (int dx = rr - 1; dx >= -rr; --dx) visit(dx, rr);
+            for (int dy = rr - 1; dy >= -rr + 1; --dy) visit(-rr, dy);
+          }
+          n_cmp += cmp;
+        } else if (RADIUS == 1) {
+          // earlier neighbours must be strictly lower, later ones not higher;
+          // out-of-image neighbours read the tile's zero margin
+          const int e0 = max(max(row[-rp - 1], row[-rp]), max(row[-rp + 1], row[-1]));
+          const int l0 = max(max(row[1], row[rp - 1]), max(row[rp], row[rp + 1]));
+          keep = e0 < s && l0 <= s;
+        } else {
+          for (int dy = -n; dy <= n && keep; ++dy)
+            for (int dx = -n; dx <= n; ++dx) {
+              const int v = row[dy * rp + dx];
+              const bool earlier = dy < 0 || (dy == 0 && dx < 0);
+              if (v > s || (v == s && earlier)) {
+                keep = false;
+                break;
               }
-          }
-          if (!keep) continue;
-          if (local_keys) {
-            // in-cell key parts from the level's table: cell << 10 | (1023 - local)
-            const uint32_t ck = __ldg(P.keytab + L.kt_col + x), rk = __ldg(P.keytab + L.kt_row + y);
-            const uint32_t key = (static_cast<uint32_t>(s) << 20) | ((rk & 1023u) << 10) | (ck & 1023u);
-            atomicMax(skeys + (static_cast<int>(rk >> 10) - cr0) * P.cols + static_cast<int>(ck >> 10),
-                      key);
-          } else {
-            const int X = x << k, Y = y << k;
-            atomicMax(P.keys + static_cast<size_t>(f) * P.cells + P.div_ch(Y) * P.cols + P.div_cw(X),
-                      pack_key(s, k, X, Y));
-          }
+            }
         }
-        if (resident) break;
+        if (!keep) continue;
+        if (local_keys) {
+          // in-cell key parts from the level's table: cell << 10 | (1023 - local)
+          const uint32_t ck = __ldg(P.keytab + L.kt_col + x), rk = __ldg(P.keytab + L.kt_row + y);
+          const uint32_t key = (static_cast<uint32_t>(s) << 20) | ((rk & 1023u) << 10) | (ck & 1023u);
+          atomicMax(skeys + (static_cast<int>(rk >> 10) - cr0) * P.cols + static_cast<int>(ck >> 10),
+                    key);
+        } else {
+          const int X = x << k, Y = y << k;
+          atomicMax(P.keys + static_cast<size_t>(f) * P.cells + P.div_ch(Y) * P.cols + P.div_cw(X),
+                    pack_key(s, k, X, Y));
+        }
       }
+      if (resident) break;
     }
-    if (P.stats) {
-      for (int o = 16; o; o >>= 1) {
-        n_cand += __shfl_xor_sync(0xffffffffu, n_cand, o);
-        n_cmp += __shfl_xor_sync(0xffffffffu, n_cmp, o);
-      }
-      if (lane == 0 && (n_cand | n_cmp)) {
-        atomicAdd(P.stats + 2 * f, n_cand);
-        atomicAdd(P.stats + 2 * f + 1, n_cmp);
-      }
+  }
+  if (P.stats) {
+    for (int o = 16; o; o >>= 1) {
+      n_cand += __shfl_xor_sync(0xffffffffu, n_cand, o);
+      n_cmp += __shfl_xor_sync(0xffffffffu, n_cmp, o);
     }
-    if (local_keys) {
-      __syncthreads();
-      // --- 6. flush the shared cell keys into the frame's global keys
-      for (int i = tid; i < slots; i += kThreads) {
-        const uint32_t key = skeys[i];
-        if (!key) continue;
-        const int ccy = cr0 + i / P.cols, ccx = i % P.cols;
-        const int ox = (ccx * P.cell_w + (1 << k) - 1) >> k;
-        const int oy = (ccy * P.cell_h + (1 << k) - 1) >> k;
-        const int y = oy + 1023 - static_cast<int>((key >> 10) & 1023u);
-        const int x = ox + 1023 - static_cast<int>(key & 1023u);
-        atomicMax(P.keys + static_cast<size_t>(f) * P.cells + i + cr0 * P.cols,
-                  pack_key(static_cast<int>(key >> 20), k, x << k, y << k));
-      }
+    if (lane == 0 && (n_cand | n_cmp)) {
+      atomicAdd(P.stats + 2 * f, n_cand);
+      atomicAdd(P.stats + 2 * f + 1, n_cmp);
     }
-    __syncthreads();  // this item is done with every shared buffer
-    if (!has_next) break;
-    item = nxt;
-    it = nx;
+  }
+  if (!local_keys) return;
+  __syncthreads();
+
+  // --- 6. flush the shared cell keys into the frame's global keys
+  for (int i = tid; i < slots; i += kThreads) {
+    const uint32_t key = skeys[i];
+    if (!key) continue;
+    const int ccy = cr0 + i / P.cols, ccx = i % P.cols;
+    const int ox = (ccx * P.cell_w + (1 << k) - 1) >> k;
+    const int oy = (ccy * P.cell_h + (1 << k) - 1) >> k;
+    const int y = oy + 1023 - static_cast<int>((key >> 10) & 1023u);
+    const int x = ox + 1023 - static_cast<int>(key & 1023u);
+    atomicMax(P.keys + static_cast<size_t>(f) * P.cells + i + cr0 * P.cols,
+              pack_key(static_cast<int>(key >> 20), k, x << k, y << k));
   }
 }
 
