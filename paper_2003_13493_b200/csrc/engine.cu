@@ -2,6 +2,7 @@
 // buffers, launch plan, stage timing, conformance and synthetic frames.
 #include <atomic>
 #include <cstddef>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <string>
@@ -200,8 +201,10 @@ fused::Params fused_geometry(const DetectParams& p, const Geometry& g, int R, in
     fused::Level& L = P.lv[k];
     L.w = g.lw[k];
     L.h = g.lh[k];
-    // u16 corner-list entries address stage columns below 1024: tiles <= 928 px
-    L.tiles_x = std::max(std::max(1, std::min(tiles0, (L.w + 63) / 64)), (L.w + 927) / 928);
+    // every level uses level 0's tile width; u16 corner-list entries address
+    // stage columns below 1024, so tiles are at most 928 px
+    const int tw0 = std::min((g.lw[0] + tiles0 - 1) / tiles0, 928);
+    L.tiles_x = (L.w + tw0 - 1) / tw0;
     L.tile_w = (L.w + L.tiles_x - 1) / L.tiles_x;
     L.tiles_x = (L.w + L.tile_w - 1) / L.tile_w;
     L.bands = (L.h + R - 1) / R;
@@ -244,13 +247,34 @@ void DeviceBatch::run(const uint8_t* frames, size_t fstride, int pitch, int coun
   int R = fused_R_;
   const int r_min = 8;
   const char* forced = std::getenv("FLKB_BAND_ROWS");  // tuning override
-  if (forced) R = std::max(4, std::atoi(forced));
-  int tiles0 = 1;
+  // u16 corner-list entries hold the band row in 6 bits: R + 2 radius <= 64
+  const int r_max = std::max(4, (64 - 2 * p_.radius) & ~3);
+  if (forced) R = std::min(r_max, std::max(4, std::atoi(forced)));
+  const char* forced_tiles = std::getenv("FLKB_TILES");  // tuning override
+  int tiles0 = forced_tiles ? std::max(1, std::atoi(forced_tiles)) : 1;
   fused::Params P = fused_geometry(p_, g_, R, tiles0);
-  // shrink the band until kMinBlocks CTAs fit one SM, then split columns
-  while (!forced && fused::smem_layout(P).total > kFusedSmemTarget && R > 16) {
-    R -= 4;
+  if (!forced && !forced_tiles && fused_tiles0_ > 0) {
+    R = fused_R_, tiles0 = fused_tiles0_;
     P = fused_geometry(p_, g_, R, tiles0);
+  } else if (!forced && !forced_tiles) {
+    // Pick (band rows, column tiles) with the least halo work among the
+    // shapes that fit kMinBlocks CTAs per SM: plane words cost ~0.3, mask
+    // words ~0.7 per row, plus a fixed per-CTA share (setup, NMS, flush).
+    double best = 1e300;
+    for (int r = std::min(r_max, 40); r >= 12; r -= 4) {
+      for (int t = 1; t <= 8; ++t) {
+        const fused::Params q = fused_geometry(p_, g_, r, t);
+        if (fused::smem_layout(q).total > kFusedSmemTarget) continue;
+        const int n = p_.radius;
+        double cost = 0;
+        for (int k = 0; k < q.levels; ++k)
+          cost += double(q.lv[k].bands) * q.lv[k].tiles_x * q.lv[k].nw *
+                  (0.3 * (r + 2 * n + 6) + 0.7 * (r + 2 * n) + 4.0);
+        if (cost < best) best = cost, R = r, tiles0 = t, P = q;
+        break;  // more tiles at the same r only add column halo
+      }
+    }
+    if (best < 1e300) fused_R_ = R, fused_tiles0_ = tiles0;
   }
   while (fused::smem_layout(P).total > kFusedSmemTarget && P.lv[0].tile_w > 64) {
     ++tiles0;
@@ -272,7 +296,9 @@ void DeviceBatch::run(const uint8_t* frames, size_t fstride, int pitch, int coun
     P = fused_geometry(p_, g_, R, tiles0);
   }
   const int smem = fused::smem_layout(P).total;
-  if (smem > kFusedSmemMax) {  // pathological radius / geometry: staged kernels
+  if (std::getenv("FLKB_DEBUG_GEOM"))
+    std::fprintf(stderr, "flkb: R=%d tiles0=%d smem=%d ctas=%d\n", R, tiles0, smem, ctas_of(P));
+  if (smem > kFusedSmemMax || R + 2 * p_.radius > 64) {  // pathological radius: staged kernels
     run_staged(frames, fstride, pitch, count, stats, s, times, first);
     return;
   }

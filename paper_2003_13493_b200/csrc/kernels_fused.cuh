@@ -37,10 +37,13 @@ namespace flkb {
 namespace fused {
 
 constexpr int kOwn = 26;       // pixels owned by one 32-bit plane word
-constexpr int kThreads = 256;
+#ifndef FLKB_THREADS
+#define FLKB_THREADS 128
+#endif
+constexpr int kThreads = FLKB_THREADS;
 constexpr int kWarps = kThreads / 32;
 #ifndef FLKB_MIN_BLOCKS
-#define FLKB_MIN_BLOCKS 3
+#define FLKB_MIN_BLOCKS 6
 #endif
 constexpr int kMinBlocks = FLKB_MIN_BLOCKS;  // CTAs per SM the register budget targets
 constexpr int kMaxLv = 16;
@@ -103,7 +106,7 @@ struct Smem {
 // several rounds.
 __host__ __device__ inline int list_capacity(const Params& p) {
   const int worst = (p.R + 2 * p.radius) * p.nw_max * kOwn;
-  const int cap = p.list_cap > 0 ? p.list_cap : 6144;  // host override (tests force rounds)
+  const int cap = p.list_cap > 0 ? p.list_cap : 24 * kThreads;  // host override (tests force rounds)
   return worst < cap ? (worst + 7) & ~7 : cap;
 }
 

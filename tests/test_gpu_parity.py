@@ -257,6 +257,32 @@ def test_radius_generic_path_large_frames(orc, n):
     assert (feats == ref).all()
 
 
+@pytest.mark.parametrize("n", [8, 31, 40])
+def test_large_radius(orc, n):
+    """Bands need R + 2n <= 64 rows; larger radii take the staged kernels."""
+    img = synth.texture(9, 320, 240)
+    cfg = dict(epsilon=8, N=9, score_kind="mt", l=2, w=1, h=2, n=n)
+    feats, extra = fl.Detector(make_config(cfg)).run(img, stats=True)
+    ref, st = orc.detect(img, oracle.make_params(**cfg))
+    assert (feats == ref).all()
+    assert extra["stats"]["nms_comparisons"] == st.comparisons
+
+
+@pytest.mark.parametrize("shape", ["60:1", "32:3", "12:5", "8:8", "20:2"])
+def test_forced_band_shapes(orc, shape, monkeypatch):
+    """Results must not depend on the band rows / column tiles the engine picks."""
+    r, t = shape.split(":")
+    monkeypatch.setenv("FLKB_BAND_ROWS", r)
+    monkeypatch.setenv("FLKB_TILES", t)
+    img = synth.noise(31, 752, 480)
+    for cfg in (dict(epsilon=10, N=9, score_kind="sad_b", l=3, w=1, h=8, n=1),
+                dict(epsilon=20, N=12, score_kind="sad_a", l=2, w=2, h=2, n=2)):
+        feats, extra = fl.Detector(make_config(cfg)).run(img, stats=True)
+        ref, st = orc.detect(img, oracle.make_params(**cfg))
+        assert (feats == ref).all()
+        assert extra["stats"]["nms_comparisons"] == st.comparisons
+
+
 def test_batch_api_with_stats_matches_single_runs():
     frames = [synth.noise(40 + f, 320, 240) for f in range(4)]
     cfg = dict(epsilon=10, N=9, score_kind="mt", l=2, w=1, h=16, n=1)
