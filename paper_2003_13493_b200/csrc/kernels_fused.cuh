@@ -538,12 +538,19 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_detect(const __grid_co
         const int c = __popc(m);
         const unsigned nz = __ballot_sync(0xffffffffu, m != 0u);
         const int mx = __reduce_max_sync(0xffffffffu, c);
-        if (2 * mx <= 3 * __popc(nz)) {
-          int p = pos;
+        if (mx <= 2 * __popc(nz)) {
+          // two bits per trip, lowest and highest, filling the word's entries
+          // from both ends (the order inside a word is free: rounds and the
+          // suppression range are word-granular); a lone last bit is written
+          // twice to the same slot
+          uint16_t* a = list + pos;
+          uint16_t* z = list + pos + c - 1;
+          const uint32_t e31 = e0 + 31u;
           while (m) {
-            const int b = __ffs(m) - 1;
-            m &= m - 1;
-            list[p++] = static_cast<uint16_t>(e0 + b);
+            const uint32_t lz = __clz(m);
+            *a++ = static_cast<uint16_t>(e0 + (__ffs(m) - 1));
+            *z-- = static_cast<uint16_t>(e31 - lz);
+            m &= (m - 1u) & ~(0x80000000u >> lz);
           }
         } else {
           unsigned z = nz;
