@@ -206,6 +206,8 @@ fused::Params fused_geometry(const DetectParams& p, const Geometry& g, int R, in
     const int tw0 = std::min((g.lw[0] + tiles0 - 1) / tiles0, 928);
     L.tiles_x = (L.w + tw0 - 1) / tw0;
     L.tile_w = (L.w + L.tiles_x - 1) / L.tiles_x;
+    // level-0 tiles start on 16-px boundaries (the fused pyramid's blocks)
+    if (k == 0 && L.tiles_x > 1) L.tile_w = (L.tile_w + 15) & ~15;
     L.tiles_x = (L.w + L.tile_w - 1) / L.tile_w;
     L.bands = (L.h + R - 1) / R;
     L.cta0 = cta;
@@ -315,6 +317,18 @@ void DeviceBatch::run(const uint8_t* frames, size_t fstride, int pitch, int coun
   unsigned long long* st =
       reinterpret_cast<unsigned long long*>(d_stats_ + 2 * static_cast<size_t>(first));
 
+  // Pyramid levels 1 (and 2) come out of the level-0 CTAs of the fused kernel
+  // (one HBM pass over level 0 instead of two) when the band and tile shape
+  // keep their 16x4 blocks aligned; the remaining levels are detected by a
+  // second launch once the pyramid exists. Small batches keep the one-launch
+  // plan: there a level-0-only launch would not fill the GPU.
+  const int ctas0 = P.lv[0].bands * P.lv[0].tiles_x;
+  const bool aligned =
+      g_.levels >= 2 && R % 4 == 0 && (P.lv[0].tiles_x == 1 || P.lv[0].tile_w % 16 == 0);
+  bool want = static_cast<long>(ctas0) * count >= 4L * 148 * fused::kMinBlocks;
+  if (const char* e = std::getenv("FLKB_FUSE_PYR")) want = std::atoi(e) != 0;  // tests / tuning
+  const int fuse_pyr = aligned && want ? std::min(2, g_.levels - 1) : 0;
+
   cudaEvent_t ev[4] = {};
   if (times) {
     for (auto& e : ev) check_cuda(cudaEventCreate(&e), "cudaEventCreate");
@@ -322,7 +336,7 @@ void DeviceBatch::run(const uint8_t* frames, size_t fstride, int pitch, int coun
   }
   if (stats) check_cuda(cudaMemsetAsync(st, 0, sizeof(uint64_t) * 2 * count, s), "memset stats");
   int launched = 0;
-  for (int k = 1; k < g_.levels; ++k) {
+  auto pyr_down = [&](int k) {
     const uint8_t* src = k == 1 ? frames : pyr + g_.loff[k - 1];
     const int sp = k == 1 ? pitch : g_.lpitch[k - 1];
     const size_t sfs = k == 1 ? fstride : g_.pyr_frame_bytes;
@@ -331,9 +345,7 @@ void DeviceBatch::run(const uint8_t* frames, size_t fstride, int pitch, int coun
     k_pyramid_down<<<grid, block, 0, s>>>(src, sp, sfs, pyr + g_.loff[k], g_.lpitch[k],
                                           g_.pyr_frame_bytes, g_.lw[k], g_.lh[k], vec_ok);
     ++launched;
-  }
-  if (times) check_cuda(cudaEventRecord(ev[1], s), "cudaEventRecord");
-  int ctas = 0;
+  };
   for (int k = 0; k < g_.levels; ++k) {
     fused::Level& L = P.lv[k];
     L.img = k == 0 ? frames : pyr + g_.loff[k];
@@ -341,7 +353,7 @@ void DeviceBatch::run(const uint8_t* frames, size_t fstride, int pitch, int coun
     L.fstride = k == 0 ? fstride : g_.pyr_frame_bytes;
     L.tma = (reinterpret_cast<uintptr_t>(L.img) % 16 == 0) && L.pitch % 16 == 0 &&
             L.fstride % 16 == 0;
-    ctas += L.bands * L.tiles_x;
+    if (k > 0 && k < 3) P.pyr_img[k] = pyr + g_.loff[k];
   }
   P.keys = keys;
   P.keytab = d_keytab_;
@@ -351,9 +363,31 @@ void DeviceBatch::run(const uint8_t* frames, size_t fstride, int pitch, int coun
     P.lv[k].kt_row = kt_row_[k];
   }
   P.stats = stats ? st : nullptr;
-  kern<<<dim3(ctas, count), fused::kThreads, smem, s>>>(P);
-  ++launched;
-  if (times) check_cuda(cudaEventRecord(ev[2], s), "cudaEventRecord");
+  // detection of levels [kb, ke) in one launch
+  auto detect = [&](int kb, int ke, int pyr_levels) {
+    P.k_begin = kb;
+    P.k_end = ke;
+    P.pyr_levels = pyr_levels;
+    int ctas = 0;
+    for (int k = kb; k < ke; ++k) {
+      P.lv[k].cta0 = ctas;
+      ctas += P.lv[k].bands * P.lv[k].tiles_x;
+    }
+    kern<<<dim3(ctas, count), fused::kThreads, smem, s>>>(P);
+    ++launched;
+  };
+  if (fuse_pyr) {
+    detect(0, 1, fuse_pyr);
+    if (times) check_cuda(cudaEventRecord(ev[1], s), "cudaEventRecord");
+    for (int k = fuse_pyr + 1; k < g_.levels; ++k) pyr_down(k);
+    if (times) check_cuda(cudaEventRecord(ev[2], s), "cudaEventRecord");
+    detect(1, g_.levels, 0);
+  } else {
+    for (int k = 1; k < g_.levels; ++k) pyr_down(k);
+    if (times) check_cuda(cudaEventRecord(ev[1], s), "cudaEventRecord");
+    if (times) check_cuda(cudaEventRecord(ev[2], s), "cudaEventRecord");
+    detect(0, g_.levels, 0);
+  }
   k_compact<<<count, 256, 0, s>>>(keys, g_.cols, g_.cells, feats, counts);
   ++launched;
   check_cuda(cudaGetLastError(), "kernel launch");
@@ -365,11 +399,18 @@ void DeviceBatch::run(const uint8_t* frames, size_t fstride, int pitch, int coun
     cudaEventElapsedTime(&a, ev[0], ev[1]);
     cudaEventElapsedTime(&b, ev[1], ev[2]);
     cudaEventElapsedTime(&c, ev[2], ev[3]);
-    // the fused kernel computes responses and suppression together: its time
-    // is reported as crf_us; nms_us is the cell compaction
-    times->pyramid_us = a * 1e3;
-    times->crf_us = b * 1e3;
-    times->nms_us = c * 1e3;
+    // The fused kernel computes responses and suppression together (and, in
+    // the two-launch plan, pyramid levels 1-2): its time is crf_us;
+    // pyramid_us is the separate downsampling launches; nms_us holds the
+    // remaining launches (the cell compaction).
+    if (fuse_pyr) {
+      times->pyramid_us = b * 1e3;
+      times->crf_us = (a + c) * 1e3;
+    } else {
+      times->pyramid_us = a * 1e3;
+      times->crf_us = c * 1e3;
+    }
+    times->nms_us = 0;
     for (auto& e : ev) cudaEventDestroy(e);
   }
 }

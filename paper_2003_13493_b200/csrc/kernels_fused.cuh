@@ -81,6 +81,11 @@ struct Level {
 struct Params {
   Level lv[kMaxLv];
   int levels;
+  int k_begin, k_end;  // levels detected by this launch (lv[k_begin].cta0 == 0)
+  // Pyramid levels 1..pyr_levels (<= 2) written by the level-0 CTAs from their
+  // staged rows (needs R % 4 == 0 and 16-px aligned column tiles); 0 = none.
+  int pyr_levels;
+  uint8_t* pyr_img[3];  // frame 0, row 0 of levels 1, 2 (index = level)
   int eps, radius, R;
   int cell_w, cell_h, cols, cells;
   FastDiv div_cw, div_ch;
@@ -306,8 +311,8 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_detect(const __grid_co
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 
   // --- which level, band and column tile
-  int k = 0;
-  while (k + 1 < P.levels && static_cast<int>(blockIdx.x) >= P.lv[k + 1].cta0) ++k;
+  int k = P.k_begin;
+  while (k + 1 < P.k_end && static_cast<int>(blockIdx.x) >= P.lv[k + 1].cta0) ++k;
   const Level& L = P.lv[k];
   const int local = blockIdx.x - L.cta0;
   const int band = L.div_tiles(local), tile = local - band * L.tiles_x;
@@ -349,15 +354,19 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_detect(const __grid_co
   row_bytes = min(row_bytes, ((w + 15) & ~15) - gx0);
   if (L.tma) {
     row_bytes &= ~15;
-    if (tid == 0) {
+    if (warp == 0) {
       const uint32_t b = static_cast<uint32_t>(__cvta_generic_to_shared(bar));
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(b));
-      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      const uint32_t bytes = static_cast<uint32_t>(row_bytes * (yb - ya));
-      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(bytes)
-                   : "memory");
-      for (int y = ya; y < yb; ++y) {
+      if (lane == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(b));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        const uint32_t bytes = static_cast<uint32_t>(row_bytes * (yb - ya));
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(bytes)
+                     : "memory");
+      }
+      __syncwarp();
+      // one row copy per lane
+      for (int y = ya + lane; y < yb; y += 32) {
         const uint32_t dst = static_cast<uint32_t>(
             __cvta_generic_to_shared(stage + (y - iy0) * P.sw + sx0));
         const uint8_t* src = frame + static_cast<size_t>(y) * L.pitch + gx0;
@@ -385,6 +394,52 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_detect(const __grid_co
           : "=r"(done)
           : "r"(b)
           : "memory");
+    }
+  }
+
+  // --- 1b. level-0 CTAs write pyramid levels 1 (and 2) of their own rows
+  //         [y0, y1) x [x_lo, x_hi) from the staged rows: each thread turns a
+  //         16x4 level-0 block into 8x2 level-1 and 4x1 level-2 pixels with the
+  //         cascaded 2x2 round-half-up mean (image.cpp:50-62)
+  if (k == 0 && P.pyr_levels > 0) {
+    const int w1 = w >> 1, h1 = h >> 1, w2 = w1 >> 1, h2 = h1 >> 1;
+    const int bxn = (x_hi - x_lo + 15) >> 4, byn = (y1 - y0 + 3) >> 2;
+    const Level& L1 = P.lv[1];
+    uint8_t* o1 = P.pyr_img[1] + f * L1.fstride;
+    uint8_t* o2 = P.pyr_levels > 1 ? P.pyr_img[2] + f * P.lv[2].fstride : nullptr;
+    for (int i = tid; i < bxn * byn; i += kThreads) {
+      const int by = i / bxn, bxi = i - by * bxn;
+      const int x = x_lo + 16 * bxi, y = y0 + 4 * by;
+      const uint8_t* sp = stage + (y - iy0) * P.sw + (x - bx0);
+      const uint4 r0 = *reinterpret_cast<const uint4*>(sp);
+      const uint4 r1 = *reinterpret_cast<const uint4*>(sp + P.sw);
+      const uint4 r2 = *reinterpret_cast<const uint4*>(sp + 2 * P.sw);
+      const uint4 r3 = *reinterpret_cast<const uint4*>(sp + 3 * P.sw);
+      const uint32_t a0 = down4(r0.x, r0.y, r1.x, r1.y), a1 = down4(r0.z, r0.w, r1.z, r1.w);
+      const uint32_t b0 = down4(r2.x, r2.y, r3.x, r3.y), b1 = down4(r2.z, r2.w, r3.z, r3.w);
+      const int X1 = x >> 1, Y1 = y >> 1;
+      auto put8 = [&](int yy, uint32_t lo, uint32_t hi) {
+        if (yy >= h1) return;
+        uint8_t* d = o1 + static_cast<size_t>(yy) * L1.pitch + X1;
+        if (X1 + 8 <= w1) {
+          *reinterpret_cast<uint2*>(d) = make_uint2(lo, hi);
+        } else {
+          for (int j = 0; X1 + j < w1; ++j)
+            d[j] = static_cast<uint8_t>((j < 4 ? lo >> (8 * j) : hi >> (8 * (j - 4))) & 0xFFu);
+        }
+      };
+      put8(Y1, a0, a1);
+      put8(Y1 + 1, b0, b1);
+      if (o2 && (y >> 2) < h2) {
+        const int X2 = x >> 2;
+        const uint32_t c = down4(a0, a1, b0, b1);
+        uint8_t* d = o2 + static_cast<size_t>(y >> 2) * P.lv[2].pitch + X2;
+        if (X2 + 4 <= w2) {
+          *reinterpret_cast<uint32_t*>(d) = c;
+        } else {
+          for (int j = 0; X2 + j < w2; ++j) d[j] = static_cast<uint8_t>((c >> (8 * j)) & 0xFFu);
+        }
+      }
     }
   }
 

@@ -33,8 +33,10 @@ def make_config(cfg):
     return c
 
 
+@pytest.mark.parametrize("fuse", ["0", "1"])
 @pytest.mark.parametrize("case", GOLDEN, ids=[c[0] for c in GOLDEN])
-def test_golden_cases_through_c_abi(golden, case):
+def test_golden_cases_through_c_abi(golden, case, fuse, monkeypatch):
+    monkeypatch.setenv("FLKB_FUSE_PYR", fuse)
     meta, arrays = golden
     name, fam, f, w, h, cfg, full = case
     m = meta[name]
@@ -55,7 +57,8 @@ def test_golden_cases_through_c_abi(golden, case):
 
 
 @pytest.mark.parametrize("seed", range(16))
-def test_random_configs_vs_oracle(orc, seed):
+def test_random_configs_vs_oracle(orc, seed, monkeypatch):
+    monkeypatch.setenv("FLKB_FUSE_PYR", str(seed % 2))
     rng = np.random.default_rng(500 + seed)
     l = int(rng.integers(1, 5))
     w = int(rng.integers(8 << (l - 1), 400))
@@ -120,8 +123,18 @@ def read_device(ptr: int, nbytes: int) -> np.ndarray:
     return torch.as_tensor(_DevBuf(ptr, nbytes), device="cuda").cpu().numpy()
 
 
-def test_pyramid_levels_match_oracle(orc):
+@pytest.mark.parametrize("fuse", ["0", "1"])
+@pytest.mark.parametrize("shape", ["", "20:1", "16:2", "12:3", "8:5"])
+def test_pyramid_levels_match_oracle(orc, fuse, shape, monkeypatch):
+    """Levels >= 1 from the standalone downsampling kernel (FLKB_FUSE_PYR=0)
+    and from the level-0 CTAs of the fused kernel (=1: levels 1-2 written from
+    the staged rows, the rest downsampled), over several band/tile shapes."""
     import torch
+    monkeypatch.setenv("FLKB_FUSE_PYR", fuse)
+    if shape:
+        r, t = shape.split(":")
+        monkeypatch.setenv("FLKB_BAND_ROWS", r)
+        monkeypatch.setenv("FLKB_TILES", t)
     W, H, L = 753, 481, 4
     frames = np.stack([synth.texture(i, W, H) for i in range(3)])
     det = fl.Detector(fl.Config(l=L, h=4))
@@ -268,12 +281,15 @@ def test_large_radius(orc, n):
     assert extra["stats"]["nms_comparisons"] == st.comparisons
 
 
-@pytest.mark.parametrize("shape", ["60:1", "32:3", "12:5", "8:8", "20:2"])
-def test_forced_band_shapes(orc, shape, monkeypatch):
-    """Results must not depend on the band rows / column tiles the engine picks."""
+@pytest.mark.parametrize("fuse", ["0", "1"])
+@pytest.mark.parametrize("shape", ["60:1", "32:3", "12:5", "8:8", "20:2", "18:2", "16:7"])
+def test_forced_band_shapes(orc, shape, fuse, monkeypatch):
+    """Results must not depend on the band rows / column tiles the engine picks,
+    nor on whether pyramid levels 1-2 come from the fused kernel."""
     r, t = shape.split(":")
     monkeypatch.setenv("FLKB_BAND_ROWS", r)
     monkeypatch.setenv("FLKB_TILES", t)
+    monkeypatch.setenv("FLKB_FUSE_PYR", fuse)
     img = synth.noise(31, 752, 480)
     for cfg in (dict(epsilon=10, N=9, score_kind="sad_b", l=3, w=1, h=8, n=1),
                 dict(epsilon=20, N=12, score_kind="sad_a", l=2, w=2, h=2, n=2)):
