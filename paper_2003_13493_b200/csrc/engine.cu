@@ -329,7 +329,7 @@ void DeviceBatch::run(const uint8_t* frames, size_t fstride, int pitch, int coun
   if (const char* e = std::getenv("FLKB_FUSE_PYR")) want = std::atoi(e) != 0;  // tests / tuning
   const int fuse_pyr = aligned && want ? std::min(2, g_.levels - 1) : 0;
 
-  cudaEvent_t ev[4] = {};
+  cudaEvent_t ev[5] = {};
   if (times) {
     for (auto& e : ev) check_cuda(cudaEventCreate(&e), "cudaEventCreate");
     check_cuda(cudaEventRecord(ev[0], s), "cudaEventRecord");
@@ -388,21 +388,23 @@ void DeviceBatch::run(const uint8_t* frames, size_t fstride, int pitch, int coun
     if (times) check_cuda(cudaEventRecord(ev[2], s), "cudaEventRecord");
     detect(0, g_.levels, 0);
   }
+  if (times) check_cuda(cudaEventRecord(ev[3], s), "cudaEventRecord");
   k_compact<<<count, 256, 0, s>>>(keys, g_.cols, g_.cells, feats, counts);
   ++launched;
   check_cuda(cudaGetLastError(), "kernel launch");
   count_launches(launched);
   if (times) {
-    check_cuda(cudaEventRecord(ev[3], s), "cudaEventRecord");
-    check_cuda(cudaEventSynchronize(ev[3]), "cudaEventSynchronize");
-    float a = 0, b = 0, c = 0;
+    check_cuda(cudaEventRecord(ev[4], s), "cudaEventRecord");
+    check_cuda(cudaEventSynchronize(ev[4]), "cudaEventSynchronize");
+    float a = 0, b = 0, c = 0, d = 0;
     cudaEventElapsedTime(&a, ev[0], ev[1]);
     cudaEventElapsedTime(&b, ev[1], ev[2]);
     cudaEventElapsedTime(&c, ev[2], ev[3]);
+    cudaEventElapsedTime(&d, ev[3], ev[4]);
     // The fused kernel computes responses and suppression together (and, in
     // the two-launch plan, pyramid levels 1-2): its time is crf_us;
-    // pyramid_us is the separate downsampling launches; nms_us holds the
-    // remaining launches (the cell compaction).
+    // pyramid_us is the separate downsampling launches; nms_us is the cell
+    // compaction.
     if (fuse_pyr) {
       times->pyramid_us = b * 1e3;
       times->crf_us = (a + c) * 1e3;
@@ -410,7 +412,7 @@ void DeviceBatch::run(const uint8_t* frames, size_t fstride, int pitch, int coun
       times->pyramid_us = a * 1e3;
       times->crf_us = c * 1e3;
     }
-    times->nms_us = 0;
+    times->nms_us = d * 1e3;
     for (auto& e : ev) cudaEventDestroy(e);
   }
 }
