@@ -405,7 +405,7 @@ def main():
                                    "achieved = the step's algorithmic bytes / the two launches' "
                                    "summed CUDA-event time",
                          "kernel_launches_per_step": 2,
-                         "kernel_us_per_launch": fused_us,
+                         "kernel_us_per_step": fused_us,
                          "kernel_share_of_step": fused_us / (fused_us + pyr_us + comp_us),
                          "other_kernels_us": {"pyramid": pyr_us, "compact": comp_us},
                          "bytes_per_frame": bytes_frame, "bytes_per_launch": bytes_frame * B,

@@ -60,6 +60,64 @@ class Conformance(ctypes.Structure):
                 ("false_positives", ctypes.c_int)]
 
 
+MODES = {"translation": 0, "translation_offset": 1, "translation_gain": 2, "full": 3}
+TRACK_DTYPE = np.dtype([("id", "<i8"), ("x", "<f8"), ("y", "<f8"), ("alpha", "<f8"),
+                        ("beta", "<f8"), ("status", "<i4"), ("live", "<i4"),
+                        ("birth_frame", "<i4"), ("_pad", "<i4")])
+
+
+class Tracker(ctypes.Structure):
+    """TrackerConfig (lk.hpp:40-48)."""
+    _fields_ = [("mode", ctypes.c_int), ("max_iterations", ctypes.c_int),
+                ("convergence_epsilon", ctypes.c_double),
+                ("min_determinant_factor", ctypes.c_double)]
+
+
+def make_tracker(param_mode="full", max_iterations=30, convergence_epsilon=0.01,
+                 min_determinant_factor=1e-6) -> Tracker:
+    if isinstance(param_mode, str):
+        param_mode = MODES[param_mode]
+    return Tracker(param_mode, max_iterations, convergence_epsilon, min_determinant_factor)
+
+
+class Patch(ctypes.Structure):
+    _fields_ = [("level", ctypes.c_int), ("patch", ctypes.c_int),
+                ("anchor_x", ctypes.c_double), ("anchor_y", ctypes.c_double),
+                ("dims", ctypes.c_int), ("values", ctypes.c_float * 256),
+                ("coeffs", ctypes.c_double * 1024), ("hessian_inv", ctypes.c_double * 16),
+                ("hessian_det", ctypes.c_double)]
+
+
+class Templates(ctypes.Structure):
+    _fields_ = [("error", ctypes.c_int), ("nlevels", ctypes.c_int), ("lv", Patch * 16)]
+
+
+class TrackResult(ctypes.Structure):
+    _fields_ = [("status", ctypes.c_int), ("warp", ctypes.c_double * 4),
+                ("iterations", ctypes.c_int)]
+
+
+class SessionCfg(ctypes.Structure):
+    """FrontendConfig (frontend.hpp:16-23)."""
+    _fields_ = [("det", Params), ("tracker", Tracker), ("target_count", ctypes.c_int),
+                ("redetect_ratio", ctypes.c_double)]
+
+
+class SessionStats(ctypes.Structure):
+    _fields_ = [("nms_comparisons", ctypes.c_uint64), ("nms_candidates", ctypes.c_uint64),
+                ("feature_count", ctypes.c_int), ("tracks_entering", ctypes.c_int),
+                ("tracks_surviving", ctypes.c_int), ("tracks_spawned", ctypes.c_int),
+                ("redetect_fired", ctypes.c_int), ("track_iterations", ctypes.c_int)]
+
+    def as_dict(self):
+        return {n: int(getattr(self, n)) for n, _ in self._fields_}
+
+
+def session_config_entries(cfg: dict) -> dict:
+    """Config-key view (config.cpp:70-131) of a session dict for the flk_* ABI."""
+    return {k: v for k, v in cfg.items() if v is not None}
+
+
 _u8p = ctypes.POINTER(ctypes.c_uint8)
 _f32p = ctypes.POINTER(ctypes.c_float)
 
@@ -181,12 +239,76 @@ class Oracle(_Base):
             raise ValueError(f"conformance rejected ({rc})")
         return c
 
+    def _levels(self, img, levels):
+        lv = self.pyramid(img, levels)
+        arr = (_u8p * levels)(*[_ptr(np.ascontiguousarray(a), _u8p) for a in lv])
+        wk = (ctypes.c_int * levels)(*[a.shape[1] for a in lv])
+        hk = (ctypes.c_int * levels)(*[a.shape[0] for a in lv])
+        return lv, arr, wk, hk
+
+    def build_template(self, img, levels: int, x0: int, y0: int, t: Tracker) -> Templates:
+        lv, arr, wk, hk = self._levels(img, levels)
+        out = Templates()
+        self.lib.orc_build_template(arr, wk, hk, levels, x0, y0, ctypes.byref(t), ctypes.byref(out))
+        return out
+
+    def track_feature(self, prev, cur, levels, x0, y0, init, t: Tracker) -> TrackResult:
+        tpl = self.build_template(prev, levels, x0, y0, t)
+        if tpl.error or tpl.nlevels == 0:
+            raise ValueError("no valid templates")
+        lv, arr, wk, hk = self._levels(cur, levels)
+        res = TrackResult()
+        ini = (ctypes.c_double * 4)(*init)
+        rc = self.lib.orc_track_feature(ctypes.byref(tpl), arr, wk, hk, levels, ini,
+                                        ctypes.byref(t), ctypes.byref(res))
+        if rc:
+            raise ValueError(f"track_feature rejected ({rc})")
+        return res
+
+    def session(self, cfg: SessionCfg):
+        return OracleSession(self, cfg)
+
     def synth(self, kind, frame: int, width: int, height: int) -> np.ndarray:
         if isinstance(kind, str):
             kind = {"noise": 0, "texture": 1}[kind]
         out = np.zeros((height, width), np.uint8)
         self.lib.orc_synth_frame(kind, ctypes.c_uint64(frame), width, height, _ptr(out, _u8p))
         return out
+
+
+class OracleSession:
+    """orc_session_*: Frontend::process_frame restated (lk_oracle.c)."""
+
+    def __init__(self, orc: Oracle, cfg: SessionCfg):
+        self.lib = orc.lib
+        self.h = ctypes.c_void_p()
+        rc = self.lib.orc_session_create(ctypes.byref(cfg), ctypes.byref(self.h))
+        if rc:
+            raise ValueError(f"session config rejected ({rc})")
+        self.cap = 2 * cfg.target_count + 16
+
+    def process(self, img, conformance: bool = False):
+        """-> (tracks as TRACK_DTYPE, stats dict[, conformance]); raises on error."""
+        img = np.ascontiguousarray(img, dtype=np.uint8)
+        h, w = img.shape
+        out = np.zeros(self.cap + 4096, TRACK_DTYPE)
+        n = ctypes.c_int()
+        st = SessionStats()
+        conf = Conformance()
+        rc = self.lib.orc_session_process(self.h, _ptr(img, _u8p), w, h,
+                                          out.ctypes.data_as(ctypes.c_void_p), len(out),
+                                          ctypes.byref(n), ctypes.byref(st),
+                                          ctypes.byref(conf) if conformance else None)
+        if rc:
+            raise ValueError(f"session frame rejected ({rc})")
+        res = (out[:n.value].copy(), st.as_dict())
+        return res + ((conf.matched, conf.subset_only, conf.false_positives),) if conformance \
+            else res
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            self.lib.orc_session_destroy(self.h)
+            self.h = None
 
 
 class Reference(_Base):
@@ -271,6 +393,28 @@ class Reference(_Base):
         if rc:
             raise ValueError(f"reference conformance rejected ({rc})")
         return c
+
+    def build_template(self, img, levels: int, x0: int, y0: int, t: Tracker) -> Templates:
+        img = np.ascontiguousarray(img, dtype=np.uint8)
+        h, w = img.shape
+        out = Templates()
+        rc = self.lib.refh_build_template(_ptr(img, _u8p), w, h, levels, x0, y0,
+                                          ctypes.byref(t), ctypes.byref(out))
+        if rc:
+            raise ValueError(f"reference build_template rejected ({rc})")
+        return out
+
+    def track_feature(self, prev, cur, levels, x0, y0, init, t: Tracker) -> TrackResult:
+        prev = np.ascontiguousarray(prev, dtype=np.uint8)
+        cur = np.ascontiguousarray(cur, dtype=np.uint8)
+        h, w = prev.shape
+        res = TrackResult()
+        ini = (ctypes.c_double * 4)(*init)
+        rc = self.lib.refh_track_feature(_ptr(prev, _u8p), _ptr(cur, _u8p), w, h, levels, x0, y0,
+                                         ini, ctypes.byref(t), ctypes.byref(res))
+        if rc:
+            raise ValueError(f"reference track_feature rejected ({rc})")
+        return res
 
     def bench(self, frames: np.ndarray, config: dict, mode: int, workers: int):
         """Seconds to run flk_detector_run over every frame (see ref_harness.cpp)."""

@@ -108,6 +108,91 @@ int orc_conformance_check(const uint8_t* img, int width, int height,
 void orc_synth_frame(int kind, uint64_t frame, int width, int height,
                      uint8_t* out);
 
+/* ---------------------------------------------------------------- tracking
+ * lk_oracle.c: restatement of src/fastlk/lk.cpp and Frontend::process_frame
+ * (src/fastlk/frontend.cpp:65-225). */
+
+enum { ORC_E_IO = 2, ORC_E_DIMENSION = 3 };
+/* ParamMode (lk.hpp:17) */
+enum { ORC_MODE_TRANSLATION = 0, ORC_MODE_TRANSLATION_OFFSET = 1, ORC_MODE_TRANSLATION_GAIN = 2,
+       ORC_MODE_FULL = 3 };
+/* TrackStatus (lk.hpp:19-25) */
+enum { ORC_TRACK_CONVERGED = 0, ORC_TRACK_DIVERGED = 1, ORC_TRACK_OUT_OF_BOUNDS = 2,
+       ORC_TRACK_SINGULAR_HESSIAN = 3, ORC_TRACK_MAX_ITERATIONS = 4 };
+/* TemplateError (lk.hpp:80) */
+enum { ORC_TPL_OK = 0, ORC_TPL_OUT_OF_BOUNDS = 1, ORC_TPL_SINGULAR = 2 };
+
+/* TrackerConfig (lk.hpp:40-48) */
+typedef struct orc_tracker {
+  int mode;
+  int max_iterations;
+  double convergence_epsilon;
+  double min_determinant_factor;
+} orc_tracker;
+
+/* PatchTemplate (lk.hpp:65-78); 16x16 patches at most, 4 parameters. */
+typedef struct orc_patch {
+  int level, patch;
+  double anchor_x, anchor_y;
+  int dims;
+  float values[256];
+  double coeffs[256 * 4];
+  double hessian_inv[16];
+  double hessian_det;
+} orc_patch;
+
+typedef struct orc_templates {
+  int error;
+  int nlevels;
+  orc_patch lv[16];
+} orc_templates;
+
+typedef struct orc_track_result {
+  int status;
+  double warp[4]; /* tx, ty, alpha, beta */
+  int iterations;
+} orc_track_result;
+
+/* FrontendConfig (frontend.hpp:16-23) */
+typedef struct orc_session_cfg {
+  orc_params det;
+  orc_tracker tracker;
+  int target_count;
+  double redetect_ratio;
+} orc_session_cfg;
+
+/* Same layout as flk_track_info (include/fastlk/fastlk.h:162-173). */
+typedef struct orc_track_info {
+  int64_t id;
+  double x, y, alpha, beta;
+  int status, live, birth_frame;
+} orc_track_info;
+
+/* The counters of flk_frame_stats (fastlk.h:106-119); no timings. */
+typedef struct orc_session_stats {
+  uint64_t nms_comparisons, nms_candidates;
+  int feature_count, tracks_entering, tracks_surviving, tracks_spawned, redetect_fired,
+      track_iterations;
+} orc_session_stats;
+
+typedef struct orc_session orc_session;
+
+void orc_default_tracker(orc_tracker* t);
+int orc_validate_tracker(const orc_tracker* t);
+int orc_param_dims(int mode);
+/* build_template (lk.cpp:147-240) on a pyramid given level by level. */
+int orc_build_template(const uint8_t* const* lv, const int* wk, const int* hk, int nlevels,
+                       int x0, int y0, const orc_tracker* cfg, orc_templates* out);
+/* track_feature (lk.cpp:242-350); init = {tx, ty, alpha, beta}. */
+int orc_track_feature(const orc_templates* tpl, const uint8_t* const* lv, const int* wk,
+                      const int* hk, int nlevels, const double* init, const orc_tracker* cfg,
+                      orc_track_result* res);
+int orc_session_create(const orc_session_cfg* cfg, orc_session** out);
+int orc_session_process(orc_session* s, const uint8_t* img, int width, int height,
+                        orc_track_info* out, int cap, int* count, orc_session_stats* stats,
+                        orc_conformance* conf);
+void orc_session_destroy(orc_session* s);
+
 #ifdef __cplusplus
 }
 #endif

@@ -16,6 +16,7 @@
 #include "fastlk/fast.hpp"
 #include "fastlk/frontend.hpp"
 #include "fastlk/image.hpp"
+#include "fastlk/lk.hpp"
 #include "fastlk/nms.hpp"
 #include "fastlk/oracle.hpp"
 #include "../oracle/fastlk_oracle.h"
@@ -292,6 +293,92 @@ __attribute__((visibility("default"))) double refh_bench(const uint8_t* frames, 
   for (auto* im : imgs) flk_image_destroy(im);
   if (features_out) *features_out = feats.load();
   return failed ? -3.0 : secs;
+}
+
+}  // extern "C"
+
+// ------------------------------------------------------------- tracking
+
+namespace {
+
+fastlk::TrackerConfig tracker_config(const orc_tracker* t) {
+  fastlk::TrackerConfig c;
+  c.mode = static_cast<fastlk::ParamMode>(t->mode);
+  c.max_iterations = t->max_iterations;
+  c.convergence_epsilon = t->convergence_epsilon;
+  c.min_determinant_factor = t->min_determinant_factor;
+  return c;
+}
+
+void to_orc(const fastlk::FeatureTemplates& in, orc_templates* out) {
+  std::memset(out, 0, sizeof *out);
+  out->error = static_cast<int>(in.error);
+  out->nlevels = static_cast<int>(in.levels.size());
+  for (size_t i = 0; i < in.levels.size(); ++i) {
+    const fastlk::PatchTemplate& t = in.levels[i];
+    orc_patch& o = out->lv[i];
+    o.level = t.level;
+    o.patch = t.patch;
+    o.anchor_x = t.anchor_x;
+    o.anchor_y = t.anchor_y;
+    o.dims = t.dims;
+    std::memcpy(o.values, t.values.data(), sizeof(float) * t.values.size());
+    std::memcpy(o.coeffs, t.coeffs.data(), sizeof(double) * t.coeffs.size());
+    for (int k = 0; k < 16; ++k) o.hessian_inv[k] = t.hessian_inv[static_cast<size_t>(k)];
+    o.hessian_det = t.hessian_det;
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+// build_template (lk.cpp:147-240) on the pyramid of img.
+__attribute__((visibility("default"))) int refh_build_template(const uint8_t* img, int w, int h,
+                                                               int levels, int x0, int y0,
+                                                               const orc_tracker* t,
+                                                               orc_templates* out) {
+  return guarded([&] {
+    fastlk::ImagePyramid pyr = fastlk::build_pyramid(to_image(img, w, h), levels);
+    fastlk::CellMax f;
+    f.x = x0;
+    f.y = y0;
+    to_orc(fastlk::build_template(pyr, f, tracker_config(t)), out);
+    return ORC_OK;
+  });
+}
+
+// Templates from the pyramid of prev at (x0, y0), tracked into the pyramid of
+// cur from init = {tx, ty, alpha, beta} with track_feature (lk.cpp:242-350).
+__attribute__((visibility("default"))) int refh_track_feature(const uint8_t* prev,
+                                                              const uint8_t* cur, int w, int h,
+                                                              int levels, int x0, int y0,
+                                                              const double* init,
+                                                              const orc_tracker* t,
+                                                              orc_track_result* res) {
+  return guarded([&] {
+    const fastlk::TrackerConfig cfg = tracker_config(t);
+    fastlk::ImagePyramid p0 = fastlk::build_pyramid(to_image(prev, w, h), levels);
+    fastlk::ImagePyramid p1 = fastlk::build_pyramid(to_image(cur, w, h), levels);
+    fastlk::CellMax f;
+    f.x = x0;
+    f.y = y0;
+    const fastlk::FeatureTemplates tpl = fastlk::build_template(p0, f, cfg);
+    if (!tpl.ok()) return ORC_E_CONFIG;
+    fastlk::WarpState ws;
+    ws.tx = init[0];
+    ws.ty = init[1];
+    ws.alpha = init[2];
+    ws.beta = init[3];
+    const fastlk::TrackResult r = fastlk::track_feature(tpl, p1, ws, cfg);
+    res->status = static_cast<int>(r.status);
+    res->warp[0] = r.warp.tx;
+    res->warp[1] = r.warp.ty;
+    res->warp[2] = r.warp.alpha;
+    res->warp[3] = r.warp.beta;
+    res->iterations = r.total_iterations();
+    return ORC_OK;
+  });
 }
 
 }  // extern "C"

@@ -44,3 +44,27 @@ GOLDEN += [
     ("N16_sada", "texture", 11, 300, 200, _cfg(epsilon=5, N=16, l=1, score_kind="sad_a"), True),
     ("ext_8x8_cells", "texture", 12, 256, 128, _cfg(l=2, cw=8, ch=8), True),
 ]
+
+
+# Tracking sessions (SURVEY §8(f) f1 + f2): (name, sequence, frames, width,
+# height, flk_config entries). Sequences come from tests/sessions.py.
+def _scfg(l=2, h=16, target=100, ratio=0.3, mode="full", iters=30, conv=0.01, **det):
+    c = dict(epsilon=10, N=9, score_kind="sad_b", l=l, w=1, h=h, n=1, target_count=target,
+             redetect_ratio=ratio, param_mode=mode, max_iterations=iters,
+             convergence_epsilon=conv)
+    c.update(det)
+    return c
+
+
+SESSIONS = [
+    ("slide_512x256_l2", "slide3", 48, 512, 256, _scfg()),
+    ("drift_320x240_l3_full", "drift", 16, 320, 240, _scfg(l=3, h=8, target=60, ratio=0.5)),
+    ("drift_translation", "drift", 10, 256, 192, _scfg(target=40, mode="translation")),
+    ("drift_offset", "drift", 10, 256, 192, _scfg(target=40, mode="translation_offset")),
+    ("drift_gain_mt", "drift", 10, 256, 192, _scfg(target=40, mode="translation_gain",
+                                                 score_kind="mt", N=10)),
+    ("slide_maxit2", "slide5", 12, 320, 192, _scfg(target=50, iters=2, conv=0.001,
+                                                   ratio=0.9)),
+    ("noise_l3_n2", "noise", 6, 256, 192, _scfg(l=3, h=8, target=40, n=2)),
+    ("c2_752x480_l3", "slide2", 8, 752, 480, _scfg(l=3, h=8, target=200, ratio=0.6)),
+]

@@ -11,7 +11,7 @@ import json, sys
 try:
     d = json.loads(open(sys.argv[2]).read().strip().splitlines()[-1])
     r = d["roofline"]
-    print(f"{sys.argv[1]:40s} fps={d['value']:.0f} detect_us={r['kernel_us_per_launch']:.1f} "
+    print(f"{sys.argv[1]:40s} fps={d['value']:.0f} detect_us={r['kernel_us_per_step']:.1f} "
           f"other={r['other_kernels_us']} e2e={d['e2e']['value']:.0f} clk={d['clocks']['sm_mhz']}")
 except Exception as e:
     print(sys.argv[1], "FAILED", e)
