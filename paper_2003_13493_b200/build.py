@@ -24,6 +24,9 @@ CSRC = os.path.join(PKG, "csrc")
 OBJ = os.path.join(PKG, "_obj")
 LIB = os.path.join(PKG, "libfastlk_b200.so")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+# fp64 LK tracker: no a*b+c contraction, so products and sums round like the
+# reference's x86-64 build (SSE2, no FMA) -- see csrc/session.cu
+NO_FMA = {"session.cu"}
 COMMON = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-fvisibility=hidden,-Wall",
           f"-I{os.path.join(ROOT, 'include')}", f"-I{CSRC}"]
 
@@ -44,6 +47,8 @@ def _compile(src: str, verbose: bool) -> str:
     obj = os.path.join(OBJ, os.path.basename(src) + ".o")
     cmd = [nvcc()] + ARCH + COMMON + os.environ.get("FLKB_NVCC_FLAGS", "").split() + [
         "-c", src, "-o", obj]
+    if os.path.basename(src) in NO_FMA:
+        cmd += ["-fmad=false"]
     if src.endswith(".cu"):
         cmd += ["-Xptxas", "-v"] if verbose else []
         cmd += ["--expt-relaxed-constexpr"]

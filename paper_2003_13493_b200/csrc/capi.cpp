@@ -19,6 +19,7 @@
 #include "../../include/fastlk_b200.h"
 #include "common.hpp"
 #include "engine.hpp"
+#include "session.hpp"
 
 namespace {
 
@@ -208,6 +209,12 @@ struct flk_detector {
   int first_height = 0;
   std::unique_ptr<FrameRunner> runner;
 };
+struct flk_session {
+  std::unique_ptr<flkb::Session> session;
+};
+struct flk_tracks {
+  std::vector<flk_track_info> items;
+};
 struct flkb_batch {
   std::unique_ptr<flkb::DeviceBatch> batch;
   int device = 0;
@@ -368,11 +375,7 @@ flk_status flk_features_get(const flk_features* features, int index, flk_feature
 
 void flk_features_destroy(flk_features* features) { delete features; }
 
-/* ------------------------------------------------ tracking (not provided) */
-
-static const char kNoTracking[] =
-    "tracking sessions are not provided by the B200 detector library "
-    "(outside the FAST + grid-NMS hot path)";
+/* --------------------------------------------------------------- tracking */
 
 const char* flk_track_status_name(flk_track_status status) {
   switch (status) {
@@ -387,23 +390,42 @@ const char* flk_track_status_name(flk_track_status status) {
 
 flk_status flk_session_create(const flk_config* config, flk_session** out) {
   if (!config || !out) return fail(FLK_E_INVALID_ARG, "config and out must not be NULL");
-  return fail(FLK_E_INTERNAL, kNoTracking);
+  return guarded([&] {
+    auto s = std::make_unique<flk_session>();
+    s->session = std::make_unique<flkb::Session>(config->cfg, current_device());
+    *out = s.release();
+    return FLK_OK;
+  });
 }
 
 flk_status flk_session_process(flk_session* session, const flk_image* image,
-                               flk_tracks** out_tracks, flk_frame_stats*, flk_conformance*) {
+                               flk_tracks** out_tracks, flk_frame_stats* stats,
+                               flk_conformance* conformance) {
   if (!session || !image || !out_tracks)
     return fail(FLK_E_INVALID_ARG, "session, image, and out_tracks must not be NULL");
-  return fail(FLK_E_INTERNAL, kNoTracking);
+  return guarded([&] {
+    auto t = std::make_unique<flk_tracks>();
+    session->session->process(image->img, &t->items, stats, conformance);
+    *out_tracks = t.release();
+    return FLK_OK;
+  });
 }
 
-void flk_session_destroy(flk_session*) {}
-int flk_tracks_count(const flk_tracks*) { return 0; }
-flk_status flk_tracks_get(const flk_tracks* tracks, int, flk_track_info* out) {
-  if (!tracks || !out) return fail(FLK_E_INVALID_ARG, "tracks and out must not be NULL");
-  return fail(FLK_E_INVALID_ARG, "track index out of range");
+void flk_session_destroy(flk_session* session) { delete session; }
+
+int flk_tracks_count(const flk_tracks* tracks) {
+  return tracks ? static_cast<int>(tracks->items.size()) : 0;
 }
-void flk_tracks_destroy(flk_tracks*) {}
+
+flk_status flk_tracks_get(const flk_tracks* tracks, int index, flk_track_info* out) {
+  if (!tracks || !out) return fail(FLK_E_INVALID_ARG, "tracks and out must not be NULL");
+  if (index < 0 || index >= static_cast<int>(tracks->items.size()))
+    return fail(FLK_E_INVALID_ARG, "track index out of range");
+  *out = tracks->items[static_cast<size_t>(index)];
+  return FLK_OK;
+}
+
+void flk_tracks_destroy(flk_tracks* tracks) { delete tracks; }
 
 /* ---------------------------------------------------------- B200 extension */
 

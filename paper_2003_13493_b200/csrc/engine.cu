@@ -238,8 +238,27 @@ fused::Params fused_geometry(const DetectParams& p, const Geometry& g, int R, in
 
 }  // namespace
 
+void DeviceBatch::build_pyramid(const uint8_t* frames, size_t fstride, int pitch, int count,
+                                cudaStream_t s, int first) {
+  if (count < 1 || first < 0 || first + count > capacity_)
+    throw InvalidArgument("batch count outside the batch capacity");
+  DeviceGuard guard(device_);
+  uint8_t* pyr = d_pyr_ ? d_pyr_ + static_cast<size_t>(first) * g_.pyr_frame_bytes : nullptr;
+  for (int k = 1; k < g_.levels; ++k) {
+    const uint8_t* src = k == 1 ? frames : pyr + g_.loff[k - 1];
+    const int sp = k == 1 ? pitch : g_.lpitch[k - 1];
+    const size_t sfs = k == 1 ? fstride : g_.pyr_frame_bytes;
+    const int vec_ok = (reinterpret_cast<uintptr_t>(src) % 16 == 0) && sp % 16 == 0 && sfs % 16 == 0;
+    dim3 block(32, 8), grid((g_.lw[k] + 255) / 256, (g_.lh[k] + 7) / 8, count);
+    k_pyramid_down<<<grid, block, 0, s>>>(src, sp, sfs, pyr + g_.loff[k], g_.lpitch[k],
+                                          g_.pyr_frame_bytes, g_.lw[k], g_.lh[k], vec_ok);
+  }
+  check_cuda(cudaGetLastError(), "pyramid launch");
+  count_launches(g_.levels - 1);
+}
+
 void DeviceBatch::run(const uint8_t* frames, size_t fstride, int pitch, int count, bool stats,
-                      cudaStream_t s, StageTimes* times, int first) {
+                      cudaStream_t s, StageTimes* times, int first, bool pyramid_ready) {
   if (count < 1 || first < 0 || first + count > capacity_)
     throw InvalidArgument("batch count " + std::to_string(count) + " outside [1, " +
                           std::to_string(capacity_) + "]");
@@ -327,7 +346,7 @@ void DeviceBatch::run(const uint8_t* frames, size_t fstride, int pitch, int coun
       g_.levels >= 2 && R % 4 == 0 && (P.lv[0].tiles_x == 1 || P.lv[0].tile_w % 16 == 0);
   bool want = static_cast<long>(ctas0) * count >= 4L * 148 * fused::kMinBlocks;
   if (const char* e = std::getenv("FLKB_FUSE_PYR")) want = std::atoi(e) != 0;  // tests / tuning
-  const int fuse_pyr = aligned && want ? std::min(2, g_.levels - 1) : 0;
+  const int fuse_pyr = aligned && want && !pyramid_ready ? std::min(2, g_.levels - 1) : 0;
 
   cudaEvent_t ev[5] = {};
   if (times) {
@@ -383,7 +402,8 @@ void DeviceBatch::run(const uint8_t* frames, size_t fstride, int pitch, int coun
     if (times) check_cuda(cudaEventRecord(ev[2], s), "cudaEventRecord");
     detect(1, g_.levels, 0);
   } else {
-    for (int k = 1; k < g_.levels; ++k) pyr_down(k);
+    if (!pyramid_ready)
+      for (int k = 1; k < g_.levels; ++k) pyr_down(k);
     if (times) check_cuda(cudaEventRecord(ev[1], s), "cudaEventRecord");
     if (times) check_cuda(cudaEventRecord(ev[2], s), "cudaEventRecord");
     detect(0, g_.levels, 0);

@@ -75,8 +75,14 @@ class DeviceBatch {
   // Enqueue detection of `count` device frames on `stream`. With `stats`
   // the per-frame counters are produced (slower kernels). With `times` the
   // call synchronizes and reports per-stage device time.
+  // With `pyramid_ready` the pyramid levels >= 1 of these frames are already
+  // in place (build_pyramid) and are not rebuilt.
   void run(const uint8_t* frames, size_t frame_stride, int pitch, int count, bool stats,
-           cudaStream_t stream, StageTimes* times = nullptr, int first = 0);
+           cudaStream_t stream, StageTimes* times = nullptr, int first = 0,
+           bool pyramid_ready = false);
+  // Pyramid levels >= 1 only (the tracking session's per-frame pyramid).
+  void build_pyramid(const uint8_t* frames, size_t frame_stride, int pitch, int count,
+                     cudaStream_t stream, int first = 0);
   // The staged pipeline (one launch per stage and level, u16 score maps in
   // HBM): the diagnostic path behind download_responses().
   void run_staged(const uint8_t* frames, size_t frame_stride, int pitch, int count, bool stats,

@@ -169,6 +169,11 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.flkb_detector_responses.argtypes = [_vp, _vp, _vp]
     lib.flkb_batch_run_device_timed.argtypes = [_vp, _vp, ctypes.c_size_t, ctypes.c_int,
                                                 ctypes.c_int, _vp, _vp]
+    lib.flk_session_create.argtypes = [_vp, ctypes.POINTER(_vp)]
+    lib.flk_session_process.argtypes = [_vp, _vp, ctypes.POINTER(_vp), _vp, _vp]
+    lib.flk_tracks_count.argtypes = [_vp]
+    lib.flk_tracks_get.argtypes = [_vp, ctypes.c_int, _vp]
+    lib.flk_track_status_name.argtypes = [ctypes.c_int]
     lib.flkb_synth_frames_device.argtypes = [_vp, ctypes.c_int, ctypes.c_uint64, ctypes.c_int,
                                              ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                              ctypes.c_size_t, _vp]
@@ -283,6 +288,48 @@ def _features_to_array(handle) -> np.ndarray:
         _check(_lib.flk_features_get(handle, i, ctypes.byref(f)))
         out[i] = (f.x, f.y, f.score, f.level, f.cell_x, f.cell_y)
     return out
+
+
+TRACK_DTYPE = np.dtype([("id", "<i8"), ("x", "<f8"), ("y", "<f8"), ("alpha", "<f8"),
+                        ("beta", "<f8"), ("status", "<i4"), ("live", "<i4"),
+                        ("birth_frame", "<i4"), ("_pad", "<i4")])
+TRACK_STATUS = ("CONVERGED", "DIVERGED", "OUT_OF_BOUNDS", "SINGULAR_HESSIAN", "MAX_ITERATIONS")
+
+
+class Session(_Handle):
+    """flk_session: the detect-track lifecycle (reference Frontend) on the GPU.
+
+    process() advances one frame and returns the live tracks plus the tracks
+    retired on this frame, ordered by id, as a TRACK_DTYPE array (the fields of
+    flk_track_info), plus the stats / conformance dicts when requested."""
+    _destroy = "flk_session_destroy"
+
+    def __init__(self, config: Config):
+        super().__init__()
+        _check(_lib.flk_session_create(config.handle, ctypes.byref(self._h)))
+
+    def process(self, image, stats: bool = False, conformance: bool = False):
+        if isinstance(image, np.ndarray):
+            image = Image.from_array(image)
+        st = FrameStats() if stats else None
+        cf = ConformanceT() if conformance else None
+        th = _vp()
+        _check(_lib.flk_session_process(self._h, image.handle, ctypes.byref(th),
+                                        ctypes.byref(st) if st is not None else None,
+                                        ctypes.byref(cf) if cf is not None else None))
+        try:
+            n = _lib.flk_tracks_count(th)
+            out = np.zeros(n, TRACK_DTYPE)
+            for i in range(n):
+                _check(_lib.flk_tracks_get(th, i, out[i:].ctypes.data))
+        finally:
+            _lib.flk_tracks_destroy(th)
+        extra = {}
+        if st is not None:
+            extra["stats"] = {k: getattr(st, k) for k, _ in FrameStats._fields_}
+        if cf is not None:
+            extra["conformance"] = {k: getattr(cf, k) for k, _ in ConformanceT._fields_}
+        return (out, extra) if extra else out
 
 
 class Detector(_Handle):
