@@ -391,6 +391,7 @@ const char* flk_track_status_name(flk_track_status status) {
 flk_status flk_session_create(const flk_config* config, flk_session** out) {
   if (!config || !out) return fail(FLK_E_INVALID_ARG, "config and out must not be NULL");
   return guarded([&] {
+    flkb::validate(config->cfg);  // config errors before the device check
     auto s = std::make_unique<flk_session>();
     s->session = std::make_unique<flkb::Session>(config->cfg, current_device());
     *out = s.release();

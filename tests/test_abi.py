@@ -184,12 +184,23 @@ def test_image_errors():
     assert "missing_file.pgm" in str(e.value)
 
 
-def test_tracking_symbols_are_explicit_stubs():
+def test_session_create_validates_before_the_device():
+    """flk_session_create: NULL checks, then the reference's config validation
+    (frontend.cpp:26-36: ratio / target -> FLK_E_CONFIG, tracker ranges ->
+    FLK_E_INVALID_ARG), then the device (no CPU fallback)."""
+    import torch
     lib = fk.load_library()
-    c = fl.Config()
     s = ctypes.c_void_p()
-    assert lib.flk_session_create(c.handle, ctypes.byref(s)) == fk.FLK_E_INTERNAL
-    assert b"not provided" in lib.flk_last_error()
+    assert lib.flk_session_create(None, ctypes.byref(s)) == fk.FLK_E_INVALID_ARG
+    for key, val, code in (("redetect_ratio", "1.0", fk.FLK_E_CONFIG),
+                           ("target_count", "0", fk.FLK_E_CONFIG),
+                           ("max_iterations", "0", fk.FLK_E_INVALID_ARG),
+                           ("convergence_epsilon", "0", fk.FLK_E_INVALID_ARG)):
+        c = fl.Config().set(key, val)
+        assert lib.flk_session_create(c.handle, ctypes.byref(s)) == code
+    if not torch.cuda.is_available():
+        assert lib.flk_session_create(fl.Config().handle, ctypes.byref(s)) == fk.FLK_E_INTERNAL
+        assert b"no CPU fallback" in lib.flk_last_error()
 
 
 def test_no_cpu_fallback_without_gpu():
