@@ -224,6 +224,103 @@ def other_configs(device: int):
     return out
 
 
+SESSION_CFG = dict(CFG, target_count=200, redetect_ratio=0.3, param_mode="full",
+                   max_iterations=30, convergence_epsilon=0.01)
+SESSION_FRAMES, SESSION_STEP = 60, 2
+
+
+def session_frames(device: int):
+    """A 752x480 sequence moving SESSION_STEP px left per frame: crops of one
+    wide S2 texture generated on the device (host copies for the host API)."""
+    import torch
+    import paper_2003_13493_b200 as fl
+    wide = W + SESSION_STEP * SESSION_FRAMES + 8
+    buf = torch.empty((H, wide), dtype=torch.uint8, device=f"cuda:{device}")
+    fl.synth_frames_device(buf.data_ptr(), 1, 77, 1, wide, H, wide, wide * H,
+                           torch.cuda.current_stream().cuda_stream)
+    master = buf.cpu().numpy()
+    return [np.ascontiguousarray(master[:, SESSION_STEP * f:SESSION_STEP * f + W])
+            for f in range(SESSION_FRAMES)]
+
+
+def session_line(device: int):
+    """SURVEY 8(f) f1+f2: the detect-track session (flk_session_process, host
+    frames in, track list out) per-frame latency on this GPU."""
+    import paper_2003_13493_b200 as fl
+    import ctypes
+    frames = session_frames(device)
+    lib = fl.load_library()
+    imgs = [fl.Image.from_array(f) for f in frames]
+    th = ctypes.c_void_p()
+
+    def run_sequence():  # raw C-ABI calls, as a C caller makes them
+        s = fl.Session(fl.Config(**SESSION_CFG))
+        ts = []
+        for im in imgs:
+            t0 = time.perf_counter()
+            assert lib.flk_session_process(s.handle, im.handle, ctypes.byref(th), None, None) == 0
+            ts.append(time.perf_counter() - t0)
+            live = lib.flk_tracks_count(th)
+            lib.flk_tracks_destroy(th)
+        return np.array(ts) * 1e6, live
+
+    run_sequence()  # warm-up (allocations, module load)
+    ts, live = run_sequence()
+    cold, ts = ts[0] / 1e6, ts[1:]
+    parts = []
+    s3 = fl.Session(fl.Config(**SESSION_CFG))
+    for f in frames:
+        _, ex = s3.process(f, stats=True)
+        parts.append((ex["stats"]["pyramid_us"], ex["stats"]["track_us"],
+                      ex["stats"]["tracks_entering"], ex["stats"]["track_iterations"]))
+    parts = np.array(parts[1:])
+    return {"workload": f"752x480 l=3 FAST-9 sad_b session, target 200 tracks, full LK "
+                        f"(translation+gain+offset), sequence moving {SESSION_STEP} px/frame, "
+                        f"{SESSION_FRAMES} frames",
+            "us_per_frame_median": float(np.median(ts)), "us_per_frame_p95": float(np.percentile(ts, 95)),
+            "frames_per_s": float(1e6 / np.median(ts)), "cold_start_us": cold * 1e6,
+            "live_tracks_last_frame": live,
+            "stage_us_median": {"pyramid": float(np.median(parts[:, 0])),
+                                "track": float(np.median(parts[:, 1]))},
+            "lk_iterations_per_track": float(parts[:, 3].sum() / max(1, parts[:, 2].sum())),
+            "includes": "H2D of the frame, pyramid, LK kernel over every live track, D2H of "
+                        "warps, host lifecycle; re-detection + template kernels when fired"}
+
+
+def session_reference(device: int):
+    """The reference's own flk_session_process (oracle/_ref) on the host on the
+    same sequence: median per-frame latency (one session, threads=0 = all cores)."""
+    import oracle
+    ref = oracle.load_reference()
+    if ref is None:
+        return None
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import sessions
+    import ctypes
+    frames = session_frames(device)
+    s = sessions.CapiSession(ref.lib, SESSION_CFG)  # sets the ctypes signatures
+    lib = ref.lib
+    imgs = []
+    for f in frames:
+        h = ctypes.c_void_p()
+        assert lib.flk_image_create(W, H, f.ctypes.data, ctypes.byref(h)) == 0
+        imgs.append(h)
+    th = ctypes.c_void_p()
+    ts = []
+    for im in imgs:  # raw C-ABI calls, as for the GPU line
+        t0 = time.perf_counter()
+        assert lib.flk_session_process(s.h, im, ctypes.byref(th), None, None) == 0
+        ts.append(time.perf_counter() - t0)
+        lib.flk_tracks_destroy(th)
+    s.close()
+    for im in imgs:
+        lib.flk_image_destroy(im)
+    ts = np.array(ts[1:]) * 1e6
+    return {"us_per_frame_median": float(np.median(ts)), "frames_per_s": float(1e6 / np.median(ts)),
+            "cores": os.cpu_count(), "kind": "reference",
+            "sample": f"{SESSION_FRAMES} frames of the same sequence, one session, threads=0"}
+
+
 def run_reference_arm(args, rank: int, world: int):
     if rank != 0:
         return
@@ -416,9 +513,12 @@ def main():
         }
         if not args.no_extras and world == 1:
             line["other_configs"] = other_configs(local)
+            line["other_configs"]["F12_session"] = session_line(local)
         if not args.no_cpu_baseline and world == 1:
             workers = os.cpu_count() or 1
             line["cpu_baseline"] = cpu_reference(min(4096, max(512, 128 * workers)), workers)
+            if "other_configs" in line:
+                line["other_configs"]["F12_session"]["cpu_baseline"] = session_reference(local)
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

@@ -118,7 +118,8 @@ __host__ __device__ inline bool has_offset(int mode) { return mode == 1 || mode 
 // gives the same accept/reject decision).
 __global__ void __launch_bounds__(256) k_template(Levels lv, const int* __restrict__ cand, int ncand,
                                                   TplLevel* __restrict__ hdr, float* __restrict__ vals,
-                                                  double* __restrict__ coef, TrackerParams tp) {
+                                                  double* __restrict__ coef, TrackerParams tp,
+                                                  int* __restrict__ tstat) {
   __shared__ double su[kMaxPx][4];
   __shared__ double hess[16];
   const int c = blockIdx.x, k = blockIdx.y, tid = threadIdx.x, L = lv.n;
@@ -127,14 +128,14 @@ __global__ void __launch_bounds__(256) k_template(Levels lv, const int* __restri
   const int w = lv.w[k], h = lv.h[k];
   const int patch = k <= 1 ? 16 : 8;
   if (w < patch + 2 || h < patch + 2) {
-    if (tid == 0) T->status = 3;
+    if (tid == 0) T->status = tstat[c * L + k] = 3;
     return;
   }
   const int half = patch / 2, npx = patch * patch, dims = tp.dims;
   const double ax = x0 / static_cast<double>(1 << k);
   const double ay = y0 / static_cast<double>(1 << k);
   if (ax - half - 1 < 0.0 || ax + half > w - 1 || ay - half - 1 < 0.0 || ay + half > h - 1) {
-    if (tid == 0) T->status = 1;
+    if (tid == 0) T->status = tstat[c * L + k] = 1;
     return;
   }
   const size_t base = (static_cast<size_t>(slot) * L + k) * kMaxPx;
@@ -177,11 +178,9 @@ __global__ void __launch_bounds__(256) k_template(Levels lv, const int* __restri
     T->dims = dims;
     T->ax = ax;
     T->ay = ay;
-    if (!(det >= tp.min_determinant_factor * area * area) || !invert_small(hm, dims, T->hinv)) {
-      T->status = 2;
-    } else {
-      T->status = 0;
-    }
+    const int st =
+        !(det >= tp.min_determinant_factor * area * area) || !invert_small(hm, dims, T->hinv) ? 2 : 0;
+    T->status = tstat[c * L + k] = st;
   }
 }
 
@@ -190,17 +189,15 @@ __global__ void __launch_bounds__(256) k_template(Levels lv, const int* __restri
 // residual and its products with the coefficients, one thread per parameter
 // sums them in pixel order, and every thread then applies the identical
 // update (deterministic, no broadcast needed).
-__global__ void __launch_bounds__(256) k_track(Levels lv, const int* __restrict__ slots,
-                                               const double* __restrict__ init,
+__global__ void __launch_bounds__(256) k_track(Levels lv, TrackIO* __restrict__ io,
                                                const TplLevel* __restrict__ hdr,
                                                const float* __restrict__ vals,
-                                               const double* __restrict__ coef, TrackerParams tp,
-                                               int* __restrict__ out_si, double* __restrict__ out_w) {
+                                               const double* __restrict__ coef, TrackerParams tp) {
   __shared__ double prod[4][kMaxPx];
   __shared__ double rhs[4];
   const int t = blockIdx.x, tid = threadIdx.x, L = lv.n;
-  const int slot = slots[t];
-  double tx0 = init[4 * t], ty0 = init[4 * t + 1], gain = init[4 * t + 2], offset = init[4 * t + 3];
+  const int slot = io[t].slot;
+  double tx0 = io[t].w[0], ty0 = io[t].w[1], gain = io[t].w[2], offset = io[t].w[3];
   int iters = 0, status = 0;
   bool aborted = false, finest_converged = false;
   int finest = -1;
@@ -271,13 +268,14 @@ __global__ void __launch_bounds__(256) k_track(Levels lv, const int* __restrict_
     if (k == finest) finest_converged = level_converged;
   }
   if (!aborted && !finest_converged) status = 4;  // MAX_ITERATIONS
+  __syncthreads();  // every thread has read io[t] before it is overwritten
   if (tid == 0) {
-    out_si[2 * t] = status;
-    out_si[2 * t + 1] = iters;
-    out_w[4 * t] = tx0;
-    out_w[4 * t + 1] = ty0;
-    out_w[4 * t + 2] = gain;
-    out_w[4 * t + 3] = offset;
+    io[t].status = status;
+    io[t].iters = iters;
+    io[t].w[0] = tx0;
+    io[t].w[1] = ty0;
+    io[t].w[2] = gain;
+    io[t].w[3] = offset;
   }
 }
 
@@ -323,9 +321,8 @@ Session::~Session() {
   cudaFree(d_hdr_);
   cudaFree(d_vals_);
   cudaFree(d_coef_);
-  cudaFree(d_ints_);
-  cudaFree(d_dbl_);
-  cudaFree(d_res_);
+  cudaFree(d_io_);
+  cudaFreeHost(h_io_);
   if (stream_) cudaStreamDestroy(stream_);
   if (cur >= 0) cudaSetDevice(cur);
 }
@@ -347,16 +344,15 @@ void Session::setup(int width, int height) {
   cudaFree(d_hdr_);
   cudaFree(d_vals_);
   cudaFree(d_coef_);
-  cudaFree(d_ints_);
-  cudaFree(d_dbl_);
-  cudaFree(d_res_);
+  cudaFree(d_io_);
+  cudaFreeHost(h_io_);
   check_cuda(cudaMalloc(&d_hdr_, per * sizeof(lk::TplLevel)), "templates");
   check_cuda(cudaMalloc(&d_vals_, per * lk::kMaxPx * sizeof(float)), "templates");
   check_cuda(cudaMalloc(&d_coef_, per * lk::kMaxPx * 4 * sizeof(double)), "templates");
-  check_cuda(cudaMalloc(&d_ints_, static_cast<size_t>(slots_) * 3 * sizeof(int)), "slots");
-  check_cuda(cudaMalloc(&d_dbl_, static_cast<size_t>(slots_) * 8 * sizeof(double)), "warps");
-  check_cuda(cudaMalloc(&d_res_, static_cast<size_t>(slots_) * 2 * sizeof(int) +
-                                     per * sizeof(int)), "results");
+  io_bytes_ = std::max(static_cast<size_t>(slots_) * sizeof(lk::TrackIO),
+                       static_cast<size_t>(slots_) * 3 * sizeof(int) + per * sizeof(int));
+  check_cuda(cudaMalloc(&d_io_, io_bytes_), "session io");
+  check_cuda(cudaMallocHost(&h_io_, io_bytes_), "session io (pinned)");
   free_.clear();
   for (int s = slots_ - 1; s >= 0; --s) free_.push_back(s);
   tracks_.clear();
@@ -413,40 +409,31 @@ void Session::process(const HostImage& img, std::vector<flk_track_info>* out,
   st.tracks_entering = static_cast<int>(tracks_.size());
   if (!tracks_.empty()) {
     const int n = static_cast<int>(tracks_.size());
-    std::vector<int> slots(n);
-    std::vector<double> init(4 * static_cast<size_t>(n));
+    lk::TrackIO* io = reinterpret_cast<lk::TrackIO*>(h_io_);
     for (int i = 0; i < n; ++i) {
-      slots[i] = tracks_[i].slot;
-      std::copy(tracks_[i].warp, tracks_[i].warp + 4, init.begin() + 4 * i);
+      std::copy(tracks_[i].warp, tracks_[i].warp + 4, io[i].w);
+      io[i].slot = tracks_[i].slot;
     }
-    check_cuda(cudaMemcpyAsync(d_ints_, slots.data(), sizeof(int) * n, cudaMemcpyHostToDevice,
-                               stream_), "H2D slots");
-    check_cuda(cudaMemcpyAsync(d_dbl_, init.data(), sizeof(double) * 4 * n,
-                               cudaMemcpyHostToDevice, stream_), "H2D warps");
-    lk::k_track<<<n, 256, 0, stream_>>>(lv, d_ints_, d_dbl_, d_hdr_, d_vals_, d_coef_, tp_, d_res_,
-                                        d_dbl_ + 4 * static_cast<size_t>(slots_));
+    const size_t bytes = sizeof(lk::TrackIO) * n;
+    check_cuda(cudaMemcpyAsync(d_io_, h_io_, bytes, cudaMemcpyHostToDevice, stream_), "H2D tracks");
+    lk::k_track<<<n, 256, 0, stream_>>>(lv, reinterpret_cast<lk::TrackIO*>(d_io_), d_hdr_, d_vals_,
+                                        d_coef_, tp_);
     check_cuda(cudaGetLastError(), "k_track");
     count_launches(1);
-    std::vector<int> si(2 * static_cast<size_t>(n));
-    std::vector<double> wout(4 * static_cast<size_t>(n));
-    check_cuda(cudaMemcpyAsync(si.data(), d_res_, sizeof(int) * 2 * n, cudaMemcpyDeviceToHost,
-                               stream_), "D2H track status");
-    check_cuda(cudaMemcpyAsync(wout.data(), d_dbl_ + 4 * static_cast<size_t>(slots_),
-                               sizeof(double) * 4 * n, cudaMemcpyDeviceToHost, stream_),
-               "D2H warps");
+    check_cuda(cudaMemcpyAsync(h_io_, d_io_, bytes, cudaMemcpyDeviceToHost, stream_), "D2H tracks");
     check_cuda(cudaStreamSynchronize(stream_), "track");
     std::vector<Track> survivors;
     survivors.reserve(tracks_.size());
     for (int i = 0; i < n; ++i) {
       Track& tr = tracks_[i];
-      const double* wv = &wout[4 * static_cast<size_t>(i)];
-      st.track_iterations += si[2 * i + 1];
-      if (si[2 * i] == FLK_TRACK_CONVERGED) {
+      const double* wv = io[i].w;
+      st.track_iterations += io[i].iters;
+      if (io[i].status == FLK_TRACK_CONVERGED) {
         std::copy(wv, wv + 4, tr.warp);
         survivors.push_back(tr);
       } else {
         retired.push_back(flk_track_info{tr.id, tr.birth.x + wv[0], tr.birth.y + wv[1], wv[2],
-                                         wv[3], si[2 * i], 0, tr.birth_frame});
+                                         wv[3], io[i].status, 0, tr.birth_frame});
         free_.push_back(tr.slot);
       }
     }
@@ -516,7 +503,7 @@ void Session::process(const HostImage& img, std::vector<flk_track_info>* out,
       // templates of every ranked candidate in one launch, then the first
       // `need` that build (frontend.cpp:197-210)
       const int nc = static_cast<int>(cands.size());
-      std::vector<int> ci(3 * static_cast<size_t>(nc));
+      int* ci = reinterpret_cast<int*>(h_io_);
       std::vector<int> cslot(nc);
       for (int i = 0; i < nc; ++i) {
         ci[2 * i] = cands[i].x;
@@ -525,20 +512,21 @@ void Session::process(const HostImage& img, std::vector<flk_track_info>* out,
         free_.pop_back();
         ci[2 * nc + i] = cslot[i];
       }
-      check_cuda(cudaMemcpyAsync(d_ints_, ci.data(), sizeof(int) * 3 * nc, cudaMemcpyHostToDevice,
-                                 stream_), "H2D candidates");
-      lk::k_template<<<dim3(nc, L), 256, 0, stream_>>>(lv, d_ints_, nc, d_hdr_, d_vals_, d_coef_,
-                                                       tp_);
+      int* d_ci = reinterpret_cast<int*>(d_io_);
+      check_cuda(cudaMemcpyAsync(d_ci, ci, sizeof(int) * 3 * nc, cudaMemcpyHostToDevice, stream_),
+                 "H2D candidates");
+      lk::k_template<<<dim3(nc, L), 256, 0, stream_>>>(lv, d_ci, nc, d_hdr_, d_vals_, d_coef_, tp_,
+                                                       d_ci + 3 * nc);
       check_cuda(cudaGetLastError(), "k_template");
       count_launches(1);
-      std::vector<lk::TplLevel> hdr(static_cast<size_t>(slots_) * L);
-      check_cuda(cudaMemcpyAsync(hdr.data(), d_hdr_, sizeof(lk::TplLevel) * hdr.size(),
-                                 cudaMemcpyDeviceToHost, stream_), "D2H templates");
+      int* ts = ci + 3 * nc;
+      check_cuda(cudaMemcpyAsync(ts, d_ci + 3 * nc, sizeof(int) * nc * L, cudaMemcpyDeviceToHost,
+                                 stream_), "D2H template status");
       check_cuda(cudaStreamSynchronize(stream_), "templates");
       for (int i = 0; i < nc; ++i) {
         bool ok = false, bad = false;
         for (int k = 0; k < L; ++k) {
-          const int s = hdr[static_cast<size_t>(cslot[i]) * L + k].status;
+          const int s = ts[i * L + k];
           ok |= s == 0;
           bad |= s == 1 || s == 2;
         }

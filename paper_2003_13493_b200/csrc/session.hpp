@@ -28,6 +28,13 @@ struct TplLevel {
   double hinv[16];
 };
 
+// Per-track record of one LK launch: initial warp and slot in, final warp,
+// status and iteration count out (one H2D and one D2H per frame).
+struct TrackIO {
+  double w[4];  // tx, ty, alpha, beta
+  int slot, status, iters, pad;
+};
+
 struct Levels {
   const uint8_t* img[kMaxLevels];
   int pitch[kMaxLevels], w[kMaxLevels], h[kMaxLevels];
@@ -74,9 +81,9 @@ class Session {
   lk::TplLevel* d_hdr_ = nullptr;
   float* d_vals_ = nullptr;
   double* d_coef_ = nullptr;
-  int* d_ints_ = nullptr;        // slots / candidate coordinates
-  double* d_dbl_ = nullptr;      // warps in / out
-  int* d_res_ = nullptr;         // status + iterations out
+  uint8_t* d_io_ = nullptr;      // TrackIO records / candidates + template statuses
+  uint8_t* h_io_ = nullptr;      // pinned mirror
+  size_t io_bytes_ = 0;
   std::vector<Track> tracks_;    // ascending id
   std::vector<int> free_;
   int64_t next_id_ = 0;
