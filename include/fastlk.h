@@ -14,10 +14,11 @@
  * implementation. There is no CPU fallback: without a usable GPU the
  * detector calls fail with FLK_E_INTERNAL and a message.
  *
- * The tracking session (flk_session_*, flk_tracks_*) is outside this
- * library's scope; those symbols exist for link compatibility and fail with
- * FLK_E_INTERNAL. Batched and device-resident entry points live in
- * fastlk_b200.h.
+ * The tracking session (flk_session_*, flk_tracks_*) runs the reference's
+ * detect-track lifecycle with the pyramid, the fp64 LK tracker, re-detection
+ * and template building on the GPU; track records (positions, gains and
+ * offsets as doubles) and counters are bit-identical to the reference.
+ * Batched and device-resident entry points live in fastlk_b200.h.
  */
 #ifndef FASTLK_B200_FASTLK_H_
 #define FASTLK_B200_FASTLK_H_
@@ -115,7 +116,11 @@ FLK_API flk_status flk_features_get(const flk_features* features, int index,
                                     flk_feature* out);
 FLK_API void flk_features_destroy(flk_features* features);
 
-/* Tracking (reference fastlk.h:149-192): link-compatible stubs only. */
+/* Tracking (reference fastlk.h:149-192; capi.cpp:298-362 -> Frontend::
+ * process_frame, frontend.cpp:65-225). The live tracks are advanced by the
+ * LK kernel, re-detection runs the fused detector on the frame's pyramid, and
+ * new templates are built by a kernel; the host keeps the reference's order
+ * of retirement, per-cell dedupe, candidate ranking and id assignment. */
 typedef struct flk_session flk_session;
 typedef struct flk_tracks flk_tracks;
 
