@@ -354,27 +354,14 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_detect(const __grid_co
   row_bytes = min(row_bytes, ((w + 15) & ~15) - gx0);
   if (L.tma) {
     row_bytes &= ~15;
-    if (warp == 0) {
+    if (tid == 0) {
       const uint32_t b = static_cast<uint32_t>(__cvta_generic_to_shared(bar));
-      if (lane == 0) {
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(b));
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        const uint32_t bytes = static_cast<uint32_t>(row_bytes * (yb - ya));
-        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(bytes)
-                     : "memory");
-      }
-      __syncwarp();
-      // one row copy per lane
-      for (int y = ya + lane; y < yb; y += 32) {
-        const uint32_t dst = static_cast<uint32_t>(
-            __cvta_generic_to_shared(stage + (y - iy0) * P.sw + sx0));
-        const uint8_t* src = frame + static_cast<size_t>(y) * L.pitch + gx0;
-        asm volatile(
-            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
-                "r"(dst), "l"(src), "r"(row_bytes), "r"(b)
-            : "memory");
-      }
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(b));
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      const uint32_t bytes = static_cast<uint32_t>(row_bytes * (yb - ya));
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(bytes)
+                   : "memory");
     }
   } else {
     for (int i = tid; i < (yb - ya) * row_bytes; i += kThreads) {
@@ -386,7 +373,18 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_detect(const __grid_co
     for (int i = tid; i < slots; i += kThreads) skeys[i] = 0u;
   __syncthreads();
   if (L.tma) {
+    // one row copy per thread (the barrier is armed), then every thread waits
+    // for the transaction count
     const uint32_t b = static_cast<uint32_t>(__cvta_generic_to_shared(bar));
+    for (int y = ya + tid; y < yb; y += kThreads) {
+      const uint32_t dst = static_cast<uint32_t>(
+          __cvta_generic_to_shared(stage + (y - iy0) * P.sw + sx0));
+      const uint8_t* src = frame + static_cast<size_t>(y) * L.pitch + gx0;
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+              "r"(dst), "l"(src), "r"(row_bytes), "r"(b)
+          : "memory");
+    }
     uint32_t done = 0;
     while (!done) {
       asm volatile(
