@@ -97,15 +97,17 @@ __device__ __forceinline__ int fast_score(int c, const int (&ring)[16], int eps)
   }
 }
 
-// 2x2 round-half-up means of two rows of 4 pixels each -> 2 output bytes.
-__device__ __forceinline__ uint32_t down2(uint32_t a, uint32_t b) {
-  uint32_t s = (a & 0x00FF00FFu) + ((a >> 8) & 0x00FF00FFu) + (b & 0x00FF00FFu) +
-               ((b >> 8) & 0x00FF00FFu);
-  s = ((s + 0x00020002u) >> 2) & 0x00FF00FFu;
-  return (s | (s >> 8)) & 0xFFFFu;
-}
+// 2x2 round-half-up means (image.cpp:50-62) of two rows of 8 pixels each
+// (a0 a1 = row 0, b0 b1 = row 1, pixel 4m+i in byte i of word m) -> 4 output
+// bytes. Byte pairs are spread into 16-bit lanes with PRMT, summed with
+// IADD3 (at most 4*255+2, no carry between lanes), and bytes 0 and 2 of the
+// lanes shifted right by 2 are the means.
 __device__ __forceinline__ uint32_t down4(uint32_t a0, uint32_t a1, uint32_t b0, uint32_t b1) {
-  return down2(a0, b0) | (down2(a1, b1) << 16);
+  const uint32_t s0 = __byte_perm(a0, 0, 0x7250) + __byte_perm(a0, 0, 0x7351) +
+                      __byte_perm(b0, 0, 0x7250) + __byte_perm(b0, 0, 0x7351) + 0x00020002u;
+  const uint32_t s1 = __byte_perm(a1, 0, 0x7250) + __byte_perm(a1, 0, 0x7351) +
+                      __byte_perm(b1, 0, 0x7250) + __byte_perm(b1, 0, 0x7351) + 0x00020002u;
+  return __byte_perm(s0 >> 2, s1 >> 2, 0x6420);
 }
 
 // cell_candidate_wins (nms.cpp:41-46) as one unsigned compare: higher score,

@@ -405,8 +405,11 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_detect(const __grid_co
     const Level& L1 = P.lv[1];
     uint8_t* o1 = P.pyr_img[1] + f * L1.fstride;
     uint8_t* o2 = P.pyr_levels > 1 ? P.pyr_img[2] + f * P.lv[2].fstride : nullptr;
+    const float inv_bxn = 1.0f / static_cast<float>(bxn);
     for (int i = tid; i < bxn * byn; i += kThreads) {
-      const int by = i / bxn, bxi = i - by * bxn;
+      // i / bxn: (i + 1/2) / bxn is at least 1/(2 bxn) from an integer, far
+      // more than the float error for i < 2^16
+      const int by = __float2int_rz((static_cast<float>(i) + 0.5f) * inv_bxn), bxi = i - by * bxn;
       const int x = x_lo + 16 * bxi, y = y0 + 4 * by;
       const uint8_t* sp = stage + (y - iy0) * P.sw + (x - bx0);
       const uint4 r0 = *reinterpret_cast<const uint4*>(sp);
