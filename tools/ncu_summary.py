@@ -47,7 +47,8 @@ def source_lines(rep):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("report")
-    ap.add_argument("--pixels-per-launch", type=float, default=0)
+    ap.add_argument("--pixels-per-launch", type=str, default="0",
+                    help="pixels of each captured launch, comma-separated (one value = all)")
     ap.add_argument("--top", type=int, default=30)
     a = ap.parse_args()
     kernels, units = raw_metrics(a.report)
@@ -61,16 +62,19 @@ def main():
             "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum",
             "smsp__thread_inst_executed_per_inst_executed.ratio",
             "launch__grid_size", "launch__block_size", "sm__cycles_elapsed.avg"]
-    for k in kernels:
-        print(f"== {k.get('Kernel Name', '?')[:100]}")
+    px = [float(v) for v in a.pixels_per_launch.split(",")]
+    for li, k in enumerate(kernels):
+        print(f"== launch {li}: {k.get('Kernel Name', '?')[:100]}")
         for m in keys:
             if m in k:
                 print(f"  {m:62s} {k[m]:>18s} {units.get(m, '')}")
-        if a.pixels_per_launch:
+        npx = px[min(li, len(px) - 1)]
+        if npx:
             wi = float(k.get("smsp__inst_executed.sum", "0").replace(",", ""))
             tr = float(k.get("smsp__thread_inst_executed_per_inst_executed.ratio", "0").replace(",", ""))
-            print(f"  warp instructions / pixel      {wi / a.pixels_per_launch:10.3f}")
-            print(f"  thread instructions / pixel    {wi * tr / a.pixels_per_launch:10.1f}")
+            print(f"  pixels in the launch           {npx:14.0f}")
+            print(f"  warp instructions / pixel      {wi / npx:10.3f}")
+            print(f"  thread instructions / pixel    {wi * tr / npx:10.1f}")
     agg = source_lines(a.report)
     tot = sum(v[0] for v in agg.values()) or 1
     ts = sum(v[1] for v in agg.values()) or 1

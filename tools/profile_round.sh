@@ -21,4 +21,4 @@ s = fl.Session(fl.Config(**bench.SESSION_CFG))
 for f in frames[:30]:
     s.process(f)
 " > gpurun_out/ncu_lk.log 2>&1
-tail -2 gpurun_out/ncu_launch.log gpurun_out/ncu_full.log gpurun_out/ncu_lk.log
+for f in gpurun_out/ncu_launch.log gpurun_out/ncu_full.log gpurun_out/ncu_lk.log; do tail -n 2 $f; done
