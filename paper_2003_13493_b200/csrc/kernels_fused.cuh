@@ -602,11 +602,18 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_detect(const __grid_co
           uint16_t* a = list + pos;
           uint16_t* z = list + pos + c - 1;
           const uint32_t e31 = e0 + 31u;
-          while (m) {
-            const uint32_t lz = __clz(m);
-            *a++ = static_cast<uint16_t>(e0 + (__ffs(m) - 1));
-            *z-- = static_cast<uint16_t>(e31 - lz);
+          while (m) {  // unrolled by two: up to four bits per trip
+            uint32_t lz = __clz(m);
+            a[0] = static_cast<uint16_t>(e0 + (__ffs(m) - 1));
+            z[0] = static_cast<uint16_t>(e31 - lz);
             m &= (m - 1u) & ~(0x80000000u >> lz);
+            if (!m) break;
+            lz = __clz(m);
+            a[1] = static_cast<uint16_t>(e0 + (__ffs(m) - 1));
+            z[-1] = static_cast<uint16_t>(e31 - lz);
+            m &= (m - 1u) & ~(0x80000000u >> lz);
+            a += 2;
+            z -= 2;
           }
         } else {
           unsigned z = nz;
