@@ -436,7 +436,7 @@ def build(ref: bool = True) -> None:
     """make -C oracle (and the reference build when its sources are present)."""
     subprocess.run(["make", "-s", "-C", HERE, "all"], check=True)
     if ref and os.path.isdir(REF_SRC):
-        subprocess.run(["make", "-s", "-C", HERE, "ref"], check=True)
+        subprocess.run(["make", "-s", "-C", HERE, "ref", "cli"], check=True)
 
 
 def load_oracle() -> Oracle:

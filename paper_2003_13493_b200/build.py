@@ -64,6 +64,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     srcs = sorted(glob.glob(os.path.join(CSRC, "*.cu")) + glob.glob(os.path.join(CSRC, "*.cpp")))
     if (not force and os.path.exists(LIB) and os.path.getmtime(LIB) >= _deps()
             and os.path.getmtime(LIB) >= os.path.getmtime(__file__)):
+        build_cli()
         return LIB
     os.makedirs(OBJ, exist_ok=True)
     with cf.ThreadPoolExecutor(max_workers=min(8, len(srcs))) as ex:
@@ -75,7 +76,25 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if res.returncode != 0:
         raise RuntimeError(f"link failed: {' '.join(cmd)}\n{res.stdout}\n{res.stderr}")
     os.replace(tmp, LIB)
+    build_cli()
     return LIB
+
+
+CLI_SRC = os.path.join(PKG, "cli", "fastlk_cli.cpp")
+CLI_BIN = os.path.join(PKG, "fastlk_b200")
+
+
+def build_cli() -> str:
+    """The sequence harness (cli/fastlk_cli.cpp) linked against the library."""
+    if (os.path.exists(CLI_BIN) and os.path.getmtime(CLI_BIN) >= os.path.getmtime(CLI_SRC)
+            and os.path.getmtime(CLI_BIN) >= os.path.getmtime(LIB)):
+        return CLI_BIN
+    cmd = ["g++", "-O2", "-std=c++17", "-Wall", "-Wextra", f"-I{os.path.join(ROOT, 'include')}",
+           CLI_SRC, f"-L{PKG}", "-lfastlk_b200", "-Wl,-rpath,$ORIGIN", "-o", CLI_BIN]
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    if res.returncode != 0:
+        raise RuntimeError(f"CLI build failed: {' '.join(cmd)}\n{res.stdout}\n{res.stderr}")
+    return CLI_BIN
 
 
 def main():
