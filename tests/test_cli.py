@@ -86,7 +86,7 @@ CASES = [
     ("detect", ["--levels", "3"]),
     ("detect", ["--levels", "2", "--oracle", "--strict"]),
     ("detect", ["--config", "CFG"]),
-    ("track", ["--levels", "2"]),
+    ("track", ["--levels", "2"]),  # target 100 > 40 cells: both fail the same way
     ("track", ["--config", "CFG", "--oracle"]),
     ("track", ["--levels", "2", "--sweep", "10,30"]),
 ]
@@ -104,13 +104,18 @@ def test_csv_identical_to_the_reference_library(seq_dir, tmp_path, cmd, opts):
     cfg.write_text("epsilon = 12\nN = 10\nscore_kind = mt\nl = 3\nh = 8\ntarget_count = 40\n"
                    "redetect_ratio = 0.6\nparam_mode = translation_gain\n")
     opts = [str(cfg) if o == "CFG" else o for o in opts]
-    outs = []
+    outs, codes = [], []
     for name, binary in (("ours", OURS), ("ref", REF)):
         out = tmp_path / f"{name}.csv"
         r = run(binary, cmd, seq_dir, "--out", out, *opts)
-        assert r.returncode == 0, (name, r.stderr)
+        codes.append((r.returncode, r.stderr.split(":")[-2].split("(")[0].strip()
+                      if r.returncode else ""))
+        if r.returncode:
+            outs.append(None)
+            continue
         if "--sweep" in opts:
             outs.append([(tmp_path / f"{name}.target{t}.csv").read_bytes() for t in (10, 30)])
         else:
             outs.append(out.read_bytes())
+    assert codes[0] == codes[1]
     assert outs[0] == outs[1]
