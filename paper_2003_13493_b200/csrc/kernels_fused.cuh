@@ -386,11 +386,11 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_detect(const __grid_co
           : "memory");
     }
     uint32_t done = 0;
-    while (!done) {
+    while (!done) {  // suspend hint: sleep in the barrier unit rather than re-issue
       asm volatile(
-          "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0; selp.u32 %0, 1, 0, p; }"
+          "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0, %2; selp.u32 %0, 1, 0, p; }"
           : "=r"(done)
-          : "r"(b)
+          : "r"(b), "r"(20000)
           : "memory");
     }
   }
