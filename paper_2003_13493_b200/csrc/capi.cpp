@@ -80,7 +80,7 @@ class FrameRunner {
     flkb::check_cuda(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking), "stream");
     pitch_ = static_cast<int>(round16(static_cast<size_t>(w)));
     flkb::check_cuda(cudaMalloc(&d_in_, static_cast<size_t>(pitch_) * h + 16), "frame buffer");
-    in_.ensure(static_cast<size_t>(w) * h);
+    in_.ensure(static_cast<size_t>(pitch_) * h);
     const int cells = batch_.geometry().cells;
     out_.ensure(sizeof(int) * 4 + sizeof(flk_feature) * static_cast<size_t>(cells) +
                 2 * sizeof(uint64_t));
@@ -99,7 +99,7 @@ class FrameRunner {
   void run(const flkb::HostImage& img, std::vector<flk_feature>* feats, flk_frame_stats* stats,
            flk_conformance* conf) {
     flkb::DeviceGuard guard(device_);
-    std::memcpy(in_.p, img.px.data(), img.px.size());
+    stage(img);
     int* counts = static_cast<int*>(out_.p);
     flk_feature* fv = reinterpret_cast<flk_feature*>(static_cast<char*>(out_.p) + 4 * sizeof(int));
     const int cells = batch_.geometry().cells;
@@ -137,16 +137,24 @@ class FrameRunner {
   // Staged run that keeps the score maps, for flkb_detector_responses.
   void responses(const flkb::HostImage& img, float* out) {
     flkb::DeviceGuard guard(device_);
-    std::memcpy(in_.p, img.px.data(), img.px.size());
+    stage(img);
     enqueue_copy_in();
     batch_.run_staged(d_in_, static_cast<size_t>(pitch_) * h_, pitch_, 1, false, stream_);
     batch_.download_responses(0, out, stream_);
   }
 
  private:
+  // The staging buffer holds the frame at the device pitch: one contiguous
+  // DMA (a pitched 2-D copy of a small frame takes the copy engine far longer).
   void enqueue_copy_in() {
-    flkb::check_cuda(cudaMemcpy2DAsync(d_in_, pitch_, in_.p, w_, w_, h_, cudaMemcpyHostToDevice,
-                                       stream_), "H2D frame");
+    flkb::check_cuda(cudaMemcpyAsync(d_in_, in_.p, static_cast<size_t>(pitch_) * h_,
+                                     cudaMemcpyHostToDevice, stream_), "H2D frame");
+  }
+  void stage(const flkb::HostImage& img) {
+    uint8_t* dst = static_cast<uint8_t*>(in_.p);
+    for (int y = 0; y < h_; ++y)
+      std::memcpy(dst + static_cast<size_t>(y) * pitch_, img.px.data() + static_cast<size_t>(y) * w_,
+                  w_);
   }
   void capture() {
     int* counts = static_cast<int*>(out_.p);

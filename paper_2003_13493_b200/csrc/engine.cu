@@ -173,7 +173,7 @@ DeviceBatch::~DeviceBatch() {
   if (cur >= 0) cudaSetDevice(cur);
 }
 
-int DeviceBatch::kernels_per_run() const { return g_.levels + 1; }
+int DeviceBatch::kernels_per_run() const { return last_launches_ ? last_launches_ : g_.levels + 1; }
 
 namespace {
 
@@ -238,23 +238,41 @@ fused::Params fused_geometry(const DetectParams& p, const Geometry& g, int R, in
 
 }  // namespace
 
+int DeviceBatch::enqueue_pyramid(const uint8_t* frames, size_t fstride, int pitch, int count,
+                                 cudaStream_t s, int first, int k0) {
+  uint8_t* pyr = d_pyr_ ? d_pyr_ + static_cast<size_t>(first) * g_.pyr_frame_bytes : nullptr;
+  int launched = 0;
+  for (int k = k0; k < g_.levels;) {
+    const uint8_t* src = k == 1 ? frames : pyr + g_.loff[k - 1];
+    const int sp = k == 1 ? pitch : g_.lpitch[k - 1];
+    const size_t sfs = k == 1 ? fstride : g_.pyr_frame_bytes;
+    const int vec_ok = (reinterpret_cast<uintptr_t>(src) % 16 == 0) && sp % 16 == 0 && sfs % 16 == 0;
+    if (k + 1 < g_.levels) {
+      dim3 block(32, 8), grid((g_.lw[k] + 255) / 256, (g_.lh[k] + 15) / 16, count);
+      k_pyramid_down2<<<grid, block, 0, s>>>(src, sp, sfs, pyr + g_.loff[k], g_.lpitch[k],
+                                             pyr + g_.loff[k + 1], g_.lpitch[k + 1],
+                                             g_.pyr_frame_bytes, g_.lw[k], g_.lh[k], g_.lw[k + 1],
+                                             g_.lh[k + 1], vec_ok);
+      k += 2;
+    } else {
+      dim3 block(32, 8), grid((g_.lw[k] + 255) / 256, (g_.lh[k] + 7) / 8, count);
+      k_pyramid_down<<<grid, block, 0, s>>>(src, sp, sfs, pyr + g_.loff[k], g_.lpitch[k],
+                                            g_.pyr_frame_bytes, g_.lw[k], g_.lh[k], vec_ok);
+      k += 1;
+    }
+    ++launched;
+  }
+  return launched;
+}
+
 void DeviceBatch::build_pyramid(const uint8_t* frames, size_t fstride, int pitch, int count,
                                 cudaStream_t s, int first) {
   if (count < 1 || first < 0 || first + count > capacity_)
     throw InvalidArgument("batch count outside the batch capacity");
   DeviceGuard guard(device_);
-  uint8_t* pyr = d_pyr_ ? d_pyr_ + static_cast<size_t>(first) * g_.pyr_frame_bytes : nullptr;
-  for (int k = 1; k < g_.levels; ++k) {
-    const uint8_t* src = k == 1 ? frames : pyr + g_.loff[k - 1];
-    const int sp = k == 1 ? pitch : g_.lpitch[k - 1];
-    const size_t sfs = k == 1 ? fstride : g_.pyr_frame_bytes;
-    const int vec_ok = (reinterpret_cast<uintptr_t>(src) % 16 == 0) && sp % 16 == 0 && sfs % 16 == 0;
-    dim3 block(32, 8), grid((g_.lw[k] + 255) / 256, (g_.lh[k] + 7) / 8, count);
-    k_pyramid_down<<<grid, block, 0, s>>>(src, sp, sfs, pyr + g_.loff[k], g_.lpitch[k],
-                                          g_.pyr_frame_bytes, g_.lw[k], g_.lh[k], vec_ok);
-  }
+  const int n = enqueue_pyramid(frames, fstride, pitch, count, s, first);
   check_cuda(cudaGetLastError(), "pyramid launch");
-  count_launches(g_.levels - 1);
+  count_launches(n);
 }
 
 void DeviceBatch::run(const uint8_t* frames, size_t fstride, int pitch, int count, bool stats,
@@ -355,16 +373,6 @@ void DeviceBatch::run(const uint8_t* frames, size_t fstride, int pitch, int coun
   }
   if (stats) check_cuda(cudaMemsetAsync(st, 0, sizeof(uint64_t) * 2 * count, s), "memset stats");
   int launched = 0;
-  auto pyr_down = [&](int k) {
-    const uint8_t* src = k == 1 ? frames : pyr + g_.loff[k - 1];
-    const int sp = k == 1 ? pitch : g_.lpitch[k - 1];
-    const size_t sfs = k == 1 ? fstride : g_.pyr_frame_bytes;
-    const int vec_ok = (reinterpret_cast<uintptr_t>(src) % 16 == 0) && sp % 16 == 0 && sfs % 16 == 0;
-    dim3 block(32, 8), grid((g_.lw[k] + 255) / 256, (g_.lh[k] + 7) / 8, count);
-    k_pyramid_down<<<grid, block, 0, s>>>(src, sp, sfs, pyr + g_.loff[k], g_.lpitch[k],
-                                          g_.pyr_frame_bytes, g_.lw[k], g_.lh[k], vec_ok);
-    ++launched;
-  };
   for (int k = 0; k < g_.levels; ++k) {
     fused::Level& L = P.lv[k];
     L.img = k == 0 ? frames : pyr + g_.loff[k];
@@ -398,12 +406,11 @@ void DeviceBatch::run(const uint8_t* frames, size_t fstride, int pitch, int coun
   if (fuse_pyr) {
     detect(0, 1, fuse_pyr);
     if (times) check_cuda(cudaEventRecord(ev[1], s), "cudaEventRecord");
-    for (int k = fuse_pyr + 1; k < g_.levels; ++k) pyr_down(k);
+    launched += enqueue_pyramid(frames, fstride, pitch, count, s, first, fuse_pyr + 1);
     if (times) check_cuda(cudaEventRecord(ev[2], s), "cudaEventRecord");
     detect(1, g_.levels, 0);
   } else {
-    if (!pyramid_ready)
-      for (int k = 1; k < g_.levels; ++k) pyr_down(k);
+    if (!pyramid_ready) launched += enqueue_pyramid(frames, fstride, pitch, count, s, first);
     if (times) check_cuda(cudaEventRecord(ev[1], s), "cudaEventRecord");
     if (times) check_cuda(cudaEventRecord(ev[2], s), "cudaEventRecord");
     detect(0, g_.levels, 0);
@@ -413,6 +420,7 @@ void DeviceBatch::run(const uint8_t* frames, size_t fstride, int pitch, int coun
   ++launched;
   check_cuda(cudaGetLastError(), "kernel launch");
   count_launches(launched);
+  last_launches_ = launched;
   if (times) {
     check_cuda(cudaEventRecord(ev[4], s), "cudaEventRecord");
     check_cuda(cudaEventSynchronize(ev[4]), "cudaEventSynchronize");

@@ -98,6 +98,11 @@ class DeviceBatch {
 
   const Geometry& geometry() const { return g_; }
   const DetectParams& params() const { return p_; }
+  // Enqueues levels [k0, levels) of the pyramid from level k0-1 (level 0 =
+  // the caller's frames): pairs of levels per k_pyramid_down2 launch, a
+  // trailing single level per k_pyramid_down. Returns the launch count.
+  int enqueue_pyramid(const uint8_t* frames, size_t frame_stride, int pitch, int count,
+                      cudaStream_t stream, int first, int k0 = 1);
   int capacity() const { return capacity_; }
   int device() const { return device_; }
   int kernels_per_run() const;
@@ -127,6 +132,7 @@ class DeviceBatch {
   int fused_tiles0_ = 0;         // level-0 column tiles of that shape (0 = not chosen yet)
   int fused_tile_w_[kMaxLevels] = {};
   int* d_conf_ = nullptr;
+  int last_launches_ = 0;        // kernels enqueued by the last run()
 };
 
 // Device synthetic generator, bit-identical to tests/synth.py.

@@ -44,6 +44,62 @@ __global__ void __launch_bounds__(256) k_pyramid_down(const uint8_t* __restrict_
   }
 }
 
+// Levels k and k+1 from level k-1 in one pass: one thread per 16x4 block of
+// the source, 8x2 level-k pixels and 4x1 level-(k+1) pixels, cascaded
+// (image.cpp:50-62: level k+1 is the mean of the rounded level-k pixels).
+__global__ void __launch_bounds__(256) k_pyramid_down2(const uint8_t* __restrict__ src,
+                                                       int spitch, size_t sfs,
+                                                       uint8_t* __restrict__ d1, int p1,
+                                                       uint8_t* __restrict__ d2, int p2, size_t dfs,
+                                                       int w1, int h1, int w2, int h2, int vec_ok) {
+  const int f = blockIdx.z;
+  const int ty = blockIdx.y * blockDim.y + threadIdx.y;     // level-k row pair, level-(k+1) row
+  const int x8 = (blockIdx.x * blockDim.x + threadIdx.x) * 8;  // first level-k column
+  if (2 * ty >= h1 || x8 >= w1) return;
+  const uint8_t* s0 = src + f * sfs + static_cast<size_t>(4 * ty) * spitch + 2 * x8;
+  uint8_t* o1 = d1 + f * dfs + static_cast<size_t>(2 * ty) * p1 + x8;
+  const bool two_rows = 2 * ty + 1 < h1;
+  uint32_t a0, a1, b0 = 0, b1 = 0;
+  if (vec_ok && x8 + 8 <= w1 && two_rows) {
+    const uint4 r0 = __ldg(reinterpret_cast<const uint4*>(s0));
+    const uint4 r1 = __ldg(reinterpret_cast<const uint4*>(s0 + spitch));
+    const uint4 r2 = __ldg(reinterpret_cast<const uint4*>(s0 + 2 * spitch));
+    const uint4 r3 = __ldg(reinterpret_cast<const uint4*>(s0 + 3 * spitch));
+    a0 = down4(r0.x, r0.y, r1.x, r1.y);
+    a1 = down4(r0.z, r0.w, r1.z, r1.w);
+    b0 = down4(r2.x, r2.y, r3.x, r3.y);
+    b1 = down4(r2.z, r2.w, r3.z, r3.w);
+    *reinterpret_cast<uint2*>(o1) = make_uint2(a0, a1);
+    *reinterpret_cast<uint2*>(o1 + p1) = make_uint2(b0, b1);
+  } else {
+    // ragged edge: byte loads, only in-range pixels
+    const int n = min(8, w1 - x8);
+    uint8_t v[2][8] = {};
+    for (int r = 0; r < (two_rows ? 2 : 1); ++r) {
+      const uint8_t* q0 = s0 + static_cast<size_t>(2 * r) * spitch;
+      const uint8_t* q1 = q0 + spitch;
+      for (int j = 0; j < n; ++j) {
+        v[r][j] = static_cast<uint8_t>((q0[2 * j] + q0[2 * j + 1] + q1[2 * j] + q1[2 * j + 1] + 2) >> 2);
+        o1[static_cast<size_t>(r) * p1 + j] = v[r][j];
+      }
+    }
+    a0 = v[0][0] | v[0][1] << 8 | v[0][2] << 16 | static_cast<uint32_t>(v[0][3]) << 24;
+    a1 = v[0][4] | v[0][5] << 8 | v[0][6] << 16 | static_cast<uint32_t>(v[0][7]) << 24;
+    b0 = v[1][0] | v[1][1] << 8 | v[1][2] << 16 | static_cast<uint32_t>(v[1][3]) << 24;
+    b1 = v[1][4] | v[1][5] << 8 | v[1][6] << 16 | static_cast<uint32_t>(v[1][7]) << 24;
+  }
+  const int x4 = x8 >> 1;
+  if (ty < h2 && x4 < w2) {  // level-(k+1) pixels need both level-k rows and columns
+    const uint32_t c = down4(a0, a1, b0, b1);
+    uint8_t* o2 = d2 + f * dfs + static_cast<size_t>(ty) * p2 + x4;
+    if (x4 + 4 <= w2) {  // pyramid rows are 16-B aligned
+      *reinterpret_cast<uint32_t*>(o2) = c;
+    } else {
+      for (int j = 0; j < 4 && x4 + j < w2; ++j) o2[j] = static_cast<uint8_t>(c >> (8 * j));
+    }
+  }
+}
+
 // ------------------------------------------------------------------- FAST
 
 template <int N, int KIND>

@@ -13,6 +13,8 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
+#include <cstdio>
 #include <cstring>
 #include <string>
 
@@ -215,6 +217,13 @@ __global__ void __launch_bounds__(256) k_track(Levels lv, TrackIO* __restrict__ 
     const double ax = T.ax, ay = T.ay;
     const double max_step = 0.5 * hypot(static_cast<double>(w), static_cast<double>(h));
     const size_t base = (static_cast<size_t>(slot) * L + k) * kMaxPx;
+    // this thread's template pixel, fixed for the level: kept in registers
+    const int oy = -half + tid / patch, ox = -half + tid % patch;
+    double tv = 0.0, u[4] = {0.0, 0.0, 0.0, 0.0};
+    if (tid < npx) {
+      tv = vals[base + tid];
+      for (int d = 0; d < dims; ++d) u[d] = coef[(base + tid) * 4 + d];
+    }
     bool level_converged = false;
     for (int iter = 0; iter < tp.max_iterations; ++iter) {
       const double bx0 = ax - half + tx;
@@ -227,10 +236,9 @@ __global__ void __launch_bounds__(256) k_track(Levels lv, TrackIO* __restrict__ 
         break;
       }
       if (tid < npx) {
-        const int oy = -half + tid / patch, ox = -half + tid % patch;
         const double sample = sample_bilinear(img, pitch, w, h, ax + ox + tx, ay + oy + ty);
-        const double r = sample - (1.0 + gain) * vals[base + tid] - offset;
-        for (int d = 0; d < dims; ++d) prod[d][tid] = coef[(base + tid) * 4 + d] * r;
+        const double r = sample - (1.0 + gain) * tv - offset;
+        for (int d = 0; d < dims; ++d) prod[d][tid] = u[d] * r;
       }
       __syncthreads();
       if (tid < dims) {
@@ -323,6 +331,8 @@ Session::~Session() {
   cudaFree(d_coef_);
   cudaFree(d_io_);
   cudaFreeHost(h_io_);
+  for (auto e : ev_)
+    if (e) cudaEventDestroy(e);
   if (stream_) cudaStreamDestroy(stream_);
   if (cur >= 0) cudaSetDevice(cur);
 }
@@ -330,12 +340,15 @@ Session::~Session() {
 void Session::setup(int width, int height) {
   DeviceGuard guard(device_);
   batch_ = std::make_unique<DeviceBatch>(p_, device_, width, height, 1);
-  if (!stream_) check_cuda(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking), "stream");
+  if (!stream_) {
+    check_cuda(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking), "stream");
+    for (auto& e : ev_) check_cuda(cudaEventCreate(&e), "event");
+  }
   pitch_ = (width + 15) & ~15;
   cudaFree(d_frame_);
   cudaFreeHost(h_frame_);
   check_cuda(cudaMalloc(&d_frame_, static_cast<size_t>(pitch_) * height + 16), "frame");
-  check_cuda(cudaMallocHost(&h_frame_, static_cast<size_t>(width) * height), "pinned frame");
+  check_cuda(cudaMallocHost(&h_frame_, static_cast<size_t>(pitch_) * height), "pinned frame");
   // live tracks <= target_count, new candidates <= cells
   const int cells = cols_ * rows_;
   slots_ = cfg_.target_count + cells;
@@ -386,14 +399,22 @@ void Session::process(const HostImage& img, std::vector<flk_track_info>* out,
   const int L = g.levels;
   flk_frame_stats st{};
 
-  // pyramid of the current frame
-  auto t0 = Clock::now();
-  std::memcpy(h_frame_, img.px.data(), img.px.size());
-  check_cuda(cudaMemcpy2DAsync(d_frame_, pitch_, h_frame_, img.width, img.width, img.height,
-                               cudaMemcpyHostToDevice, stream_), "H2D frame");
+  // One submission for the pyramid and the LK launch, one synchronisation:
+  // H2D frame -> pyramid -> H2D track records -> k_track -> D2H records.
+  // Stage times are CUDA-event device times.
+  static const bool trace = std::getenv("FLKB_SESSION_TRACE") != nullptr;
+  const auto tt0 = Clock::now();
+  // rows re-pitched on the host, then one contiguous DMA (a pitched 2-D copy
+  // of a small frame costs the copy engine several times longer)
+  for (int y = 0; y < img.height; ++y)
+    std::memcpy(h_frame_ + static_cast<size_t>(y) * pitch_,
+                img.px.data() + static_cast<size_t>(y) * img.width, img.width);
+  const auto tt1 = Clock::now();
+  check_cuda(cudaEventRecord(ev_[0], stream_), "event");
+  check_cuda(cudaMemcpyAsync(d_frame_, h_frame_, static_cast<size_t>(pitch_) * img.height,
+                             cudaMemcpyHostToDevice, stream_), "H2D frame");
   batch_->build_pyramid(d_frame_, static_cast<size_t>(pitch_) * img.height, pitch_, 1, stream_);
-  check_cuda(cudaStreamSynchronize(stream_), "pyramid");
-  st.pyramid_us = us_since(t0);
+  check_cuda(cudaEventRecord(ev_[1], stream_), "event");
   lk::Levels lv{};
   lv.n = L;
   for (int k = 0; k < L; ++k) {
@@ -402,14 +423,9 @@ void Session::process(const HostImage& img, std::vector<flk_track_info>* out,
     lv.w[k] = g.lw[k];
     lv.h[k] = g.lh[k];
   }
-
-  // advance live tracks (frontend.cpp:100-131)
-  std::vector<flk_track_info> retired;
-  t0 = Clock::now();
-  st.tracks_entering = static_cast<int>(tracks_.size());
-  if (!tracks_.empty()) {
-    const int n = static_cast<int>(tracks_.size());
-    lk::TrackIO* io = reinterpret_cast<lk::TrackIO*>(h_io_);
+  const int n = static_cast<int>(tracks_.size());
+  lk::TrackIO* io = reinterpret_cast<lk::TrackIO*>(h_io_);
+  if (n > 0) {
     for (int i = 0; i < n; ++i) {
       std::copy(tracks_[i].warp, tracks_[i].warp + 4, io[i].w);
       io[i].slot = tracks_[i].slot;
@@ -421,7 +437,29 @@ void Session::process(const HostImage& img, std::vector<flk_track_info>* out,
     check_cuda(cudaGetLastError(), "k_track");
     count_launches(1);
     check_cuda(cudaMemcpyAsync(h_io_, d_io_, bytes, cudaMemcpyDeviceToHost, stream_), "D2H tracks");
-    check_cuda(cudaStreamSynchronize(stream_), "track");
+  }
+  check_cuda(cudaEventRecord(ev_[2], stream_), "event");
+  const auto tt2 = Clock::now();
+  check_cuda(cudaStreamSynchronize(stream_), "pyramid + track");
+  if (trace) {
+    float a = 0, b = 0;
+    cudaEventElapsedTime(&a, ev_[0], ev_[1]);
+    cudaEventElapsedTime(&b, ev_[1], ev_[2]);
+    std::fprintf(stderr, "flkb session: memcpy %.1f submit %.1f wait %.1f | dev pyr %.1f trk %.1f us\n",
+                 std::chrono::duration<double, std::micro>(tt1 - tt0).count(),
+                 std::chrono::duration<double, std::micro>(tt2 - tt1).count(), us_since(tt2),
+                 a * 1e3, b * 1e3);
+  }
+  float ms_pyr = 0, ms_trk = 0;
+  cudaEventElapsedTime(&ms_pyr, ev_[0], ev_[1]);
+  cudaEventElapsedTime(&ms_trk, ev_[1], ev_[2]);
+  st.pyramid_us = ms_pyr * 1e3;
+  st.track_us = ms_trk * 1e3;
+
+  // advance live tracks (frontend.cpp:100-131)
+  std::vector<flk_track_info> retired;
+  st.tracks_entering = n;
+  if (n > 0) {
     std::vector<Track> survivors;
     survivors.reserve(tracks_.size());
     for (int i = 0; i < n; ++i) {
@@ -439,7 +477,6 @@ void Session::process(const HostImage& img, std::vector<flk_track_info>* out,
     }
     tracks_ = std::move(survivors);
   }
-  st.track_us = us_since(t0);
   st.tracks_surviving = static_cast<int>(tracks_.size());
 
   // trigger rule (frontend.cpp:133-138)
@@ -450,7 +487,7 @@ void Session::process(const HostImage& img, std::vector<flk_track_info>* out,
 
   if (st.redetect_fired) {
     // detection on the pyramid already built
-    t0 = Clock::now();
+    const auto t0 = Clock::now();
     StageTimes times;
     batch_->run(d_frame_, static_cast<size_t>(pitch_) * img.height, pitch_, 1, stats != nullptr,
                 stream_, stats ? &times : nullptr, 0, true);

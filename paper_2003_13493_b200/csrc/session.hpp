@@ -74,6 +74,7 @@ class Session {
   int device_ = 0;
   std::unique_ptr<DeviceBatch> batch_;
   cudaStream_t stream_ = nullptr;
+  cudaEvent_t ev_[3] = {nullptr, nullptr, nullptr};
   uint8_t* d_frame_ = nullptr;
   uint8_t* h_frame_ = nullptr;  // pinned staging
   int pitch_ = 0;
