@@ -178,6 +178,13 @@ __device__ __forceinline__ uint32_t shl_fma(uint32_t x, uint32_t pow2k) {
   asm("mul.lo.u32 %0, %1, %2;" : "=r"(d) : "r"(x), "r"(pow2k));
   return d;
 }
+// a * b + c on the FMA pipe (b read from the constant bank so ptxas keeps
+// the IMAD rather than strength-reducing it to a shift + add on the ALU pipe)
+__device__ __forceinline__ uint32_t mad_fma(uint32_t a, uint32_t b, uint32_t c) {
+  uint32_t d;
+  asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+  return d;
+}
 // Ring-plane shift by a (compile-time after unrolling) dx in [-3, 3]: bit b
 // of the result holds bit b + dx of x.
 __device__ __forceinline__ uint32_t shift_fma(uint32_t x, int dx, const uint32_t (&pow2)[32]) {
@@ -672,9 +679,9 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_detect(const __grid_co
         for (int i = 0; i < 16; ++i) rb[i] = sp[ring_dy(i) * P.sw + ring_dx(i)];
         uint32_t pk[4];
 #pragma unroll
-        for (int q = 0; q < 4; ++q)
-          pk[q] = __byte_perm(__byte_perm(rb[4 * q], rb[4 * q + 1], 0x0040),
-                              __byte_perm(rb[4 * q + 2], rb[4 * q + 3], 0x0040), 0x5410);
+        for (int q = 0; q < 4; ++q)  // bytes packed with IMAD (FMA pipe; the ALU pipe is the busy one)
+          pk[q] = mad_fma(rb[4 * q + 3], P.pow2[24],
+                          mad_fma(rb[4 * q + 2], P.pow2[16], mad_fma(rb[4 * q + 1], P.pow2[8], rb[4 * q])));
         sc = sad_b_packed(pk, cc, static_cast<uint32_t>(P.eps));
       } else {
         int ring[16];
