@@ -319,3 +319,61 @@ def test_batch_api_with_stats_matches_single_runs():
         assert (got == single[i][0]).all()
         assert stats[i].nms_candidates == single[i][1]["stats"]["nms_candidates"]
         assert stats[i].nms_comparisons == single[i][1]["stats"]["nms_comparisons"]
+
+
+def _full_batch_check(orc, cfg, W, H, n, sample, cell=None, kind=1):
+    """A BASELINE-sized device batch: exact parity on a sample of frames, and
+    size-independent properties on every frame (one feature per cell, cells in
+    row-major order, positive scores, levels in range, features inside the
+    frame and inside their cell)."""
+    import torch
+    c = make_config(cfg)
+    if cell:
+        c.set_cell_size_px(*cell)
+    det = fl.Detector(c)
+    batch = fl.DeviceBatch(det, W, H, n)
+    pitch = (W + 15) // 16 * 16
+    d = torch.empty((n, H, pitch), dtype=torch.uint8, device="cuda")
+    fl.synth_frames_device(d.data_ptr(), kind, 3000, n, W, H, pitch, pitch * H)
+    batch.run_device(d.data_ptr(), pitch * H, pitch, n)
+    torch.cuda.synchronize()
+    res = batch.results(n)
+    p = oracle.make_params(**cfg, cell_width_px=cell[0] if cell else 0,
+                           cell_height_px=cell[1] if cell else 0)
+    cw, ch = p.cell_width(), p.cell_height()
+    cols, rows = (W + cw - 1) // cw, (H + ch - 1) // ch
+    for f in res:
+        assert len(f) <= cols * rows
+        key = f["cell_y"].astype(np.int64) * cols + f["cell_x"]
+        assert (np.diff(key) > 0).all()
+        assert (f["score"] > 0).all() and (f["level"] >= 0).all() and (f["level"] < cfg["l"]).all()
+        assert (f["x"] // cw == f["cell_x"]).all() and (f["y"] // ch == f["cell_y"]).all()
+        assert (f["x"] < W).all() and (f["y"] < H).all()
+    rng = np.random.default_rng(n)
+    fam = {0: synth.noise, 1: synth.texture}[kind]
+    for i in sorted(set(rng.integers(0, n, sample).tolist()) | {0, n - 1}):
+        ref, _ = orc.detect(fam(3000 + i, W, H), p)
+        assert (res[i] == ref).all(), f"frame {i}"
+    return res
+
+
+@pytest.mark.parametrize("fuse", ["0", "1"])
+def test_c4_full_batch_4096(orc, fuse, monkeypatch):
+    """BASELINE configs[3]: 4096 frames of 752x480, l=3 in one device batch
+    (the bench workload), both pyramid plans."""
+    monkeypatch.setenv("FLKB_FUSE_PYR", fuse)
+    cfg = dict(epsilon=10, N=9, score_kind="sad_b", l=3, w=1, h=8, n=1)
+    res = _full_batch_check(orc, cfg, 752, 480, 4096, 12)
+    assert sum(len(f) for f in res) > 4096 * 300
+
+
+def test_c3_full_batch_256_16px_cells(orc):
+    """BASELINE configs[2]: 256 frames of 1920x1080, l=4, FAST-12, 16x16 cells."""
+    cfg = dict(epsilon=10, N=12, score_kind="sad_b", l=4, w=1, h=2, n=1)
+    _full_batch_check(orc, cfg, 1920, 1080, 256, 4, cell=(16, 16))
+
+
+def test_c5_full_batch_4k(orc):
+    """BASELINE configs[4]: 3840x2160, l=5, FAST-10 (per-GPU batch of 32)."""
+    cfg = dict(epsilon=10, N=10, score_kind="sad_b", l=5, w=1, h=2, n=1)
+    _full_batch_check(orc, cfg, 3840, 2160, 32, 2)
