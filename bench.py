@@ -62,6 +62,17 @@ def hbm_peak():
     return 6650.0, "fallback 6.65 TB/s (B200_PROFILING.md)"
 
 
+def profiled_instructions():
+    """Warp instructions per frame of the two k_detect launches (committed ncu
+    capture, profiles/traffic.json) for the issue roofline."""
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        d = json.load(open(p))
+        return d["warp_instr_per_frame"], d["instr_source"]
+    except Exception:
+        return None, None
+
+
 def profiled_traffic(frames: int):
     """DRAM bytes of the fused kernel from the committed ncu capture
     (profiles/traffic.json: per-frame dram__bytes_read + dram__bytes_write),
@@ -511,6 +522,20 @@ def main():
             "gpu_launches": int(launches),
             "clocks": clocks.summary(),
         }
+        # The path is instruction-issue bound: the same kernels
+        # against the SM issue rate (148 SMs x 4 schedulers x 1 warp-instr/clk
+        # at the live SM clock), from the committed ncu instruction count.
+        wipf, wsrc = profiled_instructions()
+        mhz = line["clocks"].get("sm_mhz") or 1965.0
+        if wipf:
+            peak_i = 148 * 4 * mhz * 1e6 / 1e9
+            kern_i = B * wipf / (fused_us / 1e6) / 1e9
+            line["issue_roofline"] = {
+                "bound": "issue", "unit": "G warp-instr/s", "achieved": kern_i, "peak": peak_i,
+                "frac": kern_i / peak_i, "warp_instr_per_frame": wipf,
+                "note": "k_detect warp instructions per frame (ncu) x frames per launch / the "
+                        "two launches' CUDA-event time, against 148 SMs x 4 issue slots x SM clock",
+                "source": wsrc}
         if not args.no_extras and world == 1:
             line["other_configs"] = other_configs(local)
             line["other_configs"]["F12_session"] = session_line(local)
