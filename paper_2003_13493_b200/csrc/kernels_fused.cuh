@@ -30,6 +30,7 @@
 #pragma once
 
 #include <cstdint>
+#include <type_traits>
 
 #include "fast_math.cuh"
 
@@ -702,6 +703,8 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_detect(const __grid_co
     const int e_lo = T1 > T0 ? scan[kWarps + 1] : 0;
     const int e_hi = T1 > T0 ? scan[kWarps + 2] : 0;
     const int rp = P.rp;
+    const uint32_t* ktc = P.keytab + L.kt_col;  // this level's column / row key tables
+    const uint32_t* ktr = P.keytab + L.kt_row;
     for (int w0 = e_lo; w0 < e_hi; w0 += cap) {
       const bool resident = total <= cap;  // the scoring list is still in place
       const int off = resident ? 0 : w0;
@@ -711,63 +714,75 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_detect(const __grid_co
         __syncthreads();
       }
       const int m_end = resident ? e_hi : min(w0 + cap, e_hi);
-      for (int e = w0 + tid; e < m_end; e += kThreads) {
-        const int ent = list[e - off];
-        const int y = cy_lo + (ent >> 10), xs = ent & 1023;
-        const int x = bx0 + xs;
-        if (x < nx_lo || x >= nx_hi) continue;  // halo column of a neighbouring tile
-        const uint16_t* row = tile_s + (y - fy0) * rp + xs + tcol;
-        const int s = row[0];
-        if (s == 0) continue;  // a corner whose score is 0 (MT, eps 0) is no candidate
-        bool keep = true;
-        if (P.stats) {
-          ++n_cand;
-          uint32_t cmp = 0;
-          for (int rr = 1; rr <= n && keep; ++rr) {
-            auto visit = [&](int dx, int dy) {
-              if (!keep) return;
-              const int nx = x + dx, ny = y + dy;
-              if (nx < 0 || ny < 0 || nx >= w || ny >= h) return;
-              ++cmp;
-              const int v = row[dy * rp + dx];
-              if (v > s || (v == s && (dy < 0 || (dy == 0 && dx < 0)))) keep = false;
-            };
-            for (int dx = -rr; dx <= rr; ++dx) visit(dx, -rr);
-            for (int dy = -rr + 1; dy <= rr; ++dy) visit(rr, dy);
-            for (int dx = rr - 1; dx >= -rr; --dx) visit(dx, rr);
-            for (int dy = rr - 1; dy >= -rr + 1; --dy) visit(-rr, dy);
-          }
-          n_cmp += cmp;
-        } else if (RADIUS == 1) {
-          // earlier neighbours must be strictly lower, later ones not higher;
-          // out-of-image neighbours read the tile's zero margin
-          const int e0 = max(max(row[-rp - 1], row[-rp]), max(row[-rp + 1], row[-1]));
-          const int l0 = max(max(row[1], row[rp - 1]), max(row[rp], row[rp + 1]));
-          keep = e0 < s && l0 <= s;
-        } else {
-          for (int dy = -n; dy <= n && keep; ++dy)
-            for (int dx = -n; dx <= n; ++dx) {
-              const int v = row[dy * rp + dx];
-              const bool earlier = dy < 0 || (dy == 0 && dx < 0);
-              if (v > s || (v == s && earlier)) {
-                keep = false;
-                break;
-              }
+      // the loop is instantiated with and without the counters, so the
+      // fast path carries no per-candidate stats test
+      auto suppress = [&](auto with_stats) {
+        constexpr bool STATS = decltype(with_stats)::value;
+        for (int e = w0 + tid; e < m_end; e += kThreads) {
+          const int ent = list[e - off];
+          const int y = cy_lo + (ent >> 10), xs = ent & 1023;
+          const int x = bx0 + xs;
+          if (x < nx_lo || x >= nx_hi) continue;  // halo column of a neighbouring tile
+          const uint16_t* row = tile_s + (y - fy0) * rp + xs + tcol;
+          const int s = row[0];
+          if (s == 0) continue;  // a corner whose score is 0 (MT, eps 0) is no candidate
+          if constexpr (STATS) {
+            bool keep = true;
+            ++n_cand;
+            uint32_t cmp = 0;
+            for (int rr = 1; rr <= n && keep; ++rr) {
+              auto visit = [&](int dx, int dy) {
+                if (!keep) return;
+                const int nx = x + dx, ny = y + dy;
+                if (nx < 0 || ny < 0 || nx >= w || ny >= h) return;
+                ++cmp;
+                const int v = row[dy * rp + dx];
+                if (v > s || (v == s && (dy < 0 || (dy == 0 && dx < 0)))) keep = false;
+              };
+              for (int dx = -rr; dx <= rr; ++dx) visit(dx, -rr);
+              for (int dy = -rr + 1; dy <= rr; ++dy) visit(rr, dy);
+              for (int dx = rr - 1; dx >= -rr; --dx) visit(dx, rr);
+              for (int dy = rr - 1; dy >= -rr + 1; --dy) visit(-rr, dy);
             }
+            n_cmp += cmp;
+            if (!keep) continue;
+          } else if (RADIUS == 1) {
+            // earlier neighbours must be strictly lower, later ones not higher;
+            // out-of-image neighbours read the tile's zero margin
+            const int e0 = max(max(row[-rp - 1], row[-rp]), max(row[-rp + 1], row[-1]));
+            const int l0 = max(max(row[1], row[rp - 1]), max(row[rp], row[rp + 1]));
+            if (e0 >= s || l0 > s) continue;
+          } else {
+            bool keep = true;
+            for (int dy = -n; dy <= n && keep; ++dy)
+              for (int dx = -n; dx <= n; ++dx) {
+                const int v = row[dy * rp + dx];
+                const bool earlier = dy < 0 || (dy == 0 && dx < 0);
+                if (v > s || (v == s && earlier)) {
+                  keep = false;
+                  break;
+                }
+              }
+            if (!keep) continue;
+          }
+          if (local_keys) {
+            // in-cell key parts from the level's table: cell << 10 | (1023 - local)
+            const uint32_t ck = __ldg(ktc + static_cast<uint32_t>(x));
+            const uint32_t rk = __ldg(ktr + static_cast<uint32_t>(y));
+            const uint32_t key = (static_cast<uint32_t>(s) << 20) | ((rk & 1023u) << 10) | (ck & 1023u);
+            atomicMax(skeys + (static_cast<int>(rk >> 10) - cr0) * P.cols + static_cast<int>(ck >> 10),
+                      key);
+          } else {
+            const int X = x << k, Y = y << k;
+            atomicMax(P.keys + static_cast<size_t>(f) * P.cells + P.div_ch(Y) * P.cols + P.div_cw(X),
+                      pack_key(s, k, X, Y));
+          }
         }
-        if (!keep) continue;
-        if (local_keys) {
-          // in-cell key parts from the level's table: cell << 10 | (1023 - local)
-          const uint32_t ck = __ldg(P.keytab + L.kt_col + x), rk = __ldg(P.keytab + L.kt_row + y);
-          const uint32_t key = (static_cast<uint32_t>(s) << 20) | ((rk & 1023u) << 10) | (ck & 1023u);
-          atomicMax(skeys + (static_cast<int>(rk >> 10) - cr0) * P.cols + static_cast<int>(ck >> 10),
-                    key);
-        } else {
-          const int X = x << k, Y = y << k;
-          atomicMax(P.keys + static_cast<size_t>(f) * P.cells + P.div_ch(Y) * P.cols + P.div_cw(X),
-                    pack_key(s, k, X, Y));
-        }
-      }
+      };
+      if (P.stats)
+        suppress(std::true_type{});
+      else
+        suppress(std::false_type{});
       if (resident) break;
     }
   }
