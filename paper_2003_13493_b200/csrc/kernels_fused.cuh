@@ -543,8 +543,17 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_detect(const __grid_co
   const int tasks_f = max(fast_rows, 0) * nw;
   const int per = (tasks_f + kThreads - 1) / kThreads;
   const int tb = min(tid * per, tasks_f), te = min(tb + per, tasks_f);
-  int cnt = 0;
-  for (int t = tb; t < te; ++t) cnt += __popc(cm[t]);
+  // List range of the suppressed rows [y0, y1): tasks [T0, T1) are row-major,
+  // so their corners are entries [e_lo, e_hi); the owner of task T notes its
+  // local offset while counting and records the list index after the scan.
+  const int T0 = min(max(max(y0, 3) - cy_lo, 0) * nw, tasks_f);
+  const int T1 = min(max(min(y1, h - 3) - cy_lo, 0) * nw, tasks_f);
+  int cnt = 0, pre0 = -1, pre1 = -1;
+  for (int t = tb; t < te; ++t) {
+    if (t == T0) pre0 = cnt;
+    if (t == T1) pre1 = cnt;
+    cnt += __popc(cm[t]);
+  }
   {
     uint4* z = reinterpret_cast<uint4*>(tile_s);
     const int n16 = ((P.R + 2 * n) * P.rp * 2) / 16;
@@ -572,19 +581,9 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_detect(const __grid_co
   __syncthreads();
   const int base = scan[warp] + incl - cnt;  // this thread's first list index
   const int total = scan[kWarps];
-  // List range of the suppressed rows [y0, y1): tasks [T0, T1) are row-major,
-  // so their corners are entries [e_lo, e_hi); the owner of task T records
-  // its list index (read after the scoring barrier).
-  const int T0 = min(max(max(y0, 3) - cy_lo, 0) * nw, tasks_f);
-  const int T1 = min(max(min(y1, h - 3) - cy_lo, 0) * nw, tasks_f);
-  if (tb < te) {
-    int pos = base;
-    for (int t = tb; t < te; ++t) {
-      if (t == T0) scan[kWarps + 1] = pos;
-      if (t == T1) scan[kWarps + 2] = pos;
-      pos += __popc(cm[t]);
-    }
-  }
+  // (read after the scoring barrier)
+  if (pre0 >= 0) scan[kWarps + 1] = base + pre0;
+  if (pre1 >= 0) scan[kWarps + 2] = base + pre1;
   const int cap = list_capacity(P);
   const int row_tb = L.div_nw(tb), j_tb = tb - row_tb * nw;
   // Writes the entries with list index in [w0, w0 + cap) to list[index - w0].
