@@ -483,16 +483,19 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_detect(const __grid_co
     for (int t = tid; t < tasks; t += kThreads, it.next()) {
       const int y = cy_lo + it.row, j = it.j;
       const int r = y - iy0;  // stage/plane row of the centre
-      const uint32_t* base = planes + j * 4;
-      auto row_planes = [&](int rr, uint32_t (&q)[8]) {
-        const uint32_t* q4 = base + rr * P.nw_max * 4;
-        const uint4 u = *reinterpret_cast<const uint4*>(q4);
-        const uint4 v = *reinterpret_cast<const uint4*>(q4 + half);
+      // plane rows r-3..r+3 of word j: two pointers (low / high plane halves)
+      // bumped by one row per step, no per-row multiply
+      const int stride = P.nw_max * 4;
+      const uint32_t* pl = planes + j * 4 + (r - 3) * stride;
+      const uint32_t* ph = pl + half;
+      auto load_planes = [&](const uint32_t* a, const uint32_t* b, uint32_t (&q)[8]) {
+        const uint4 u = *reinterpret_cast<const uint4*>(a);
+        const uint4 v = *reinterpret_cast<const uint4*>(b);
         q[0] = u.x; q[1] = u.y; q[2] = u.z; q[3] = u.w;
         q[4] = v.x; q[5] = v.y; q[6] = v.z; q[7] = v.w;
       };
       uint32_t c[8], lo[8], hi[8];
-      row_planes(r, c);
+      load_planes(pl + 3 * stride, ph + 3 * stride, c);
       {
         uint32_t br = 0, cy = 0;
 #pragma unroll
@@ -511,9 +514,9 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_detect(const __grid_co
       }
       uint32_t dk[16], bk[16];
 #pragma unroll
-      for (int dy = -3; dy <= 3; ++dy) {
+      for (int dy = -3; dy <= 3; ++dy, pl += stride, ph += stride) {
         uint32_t q[8];
-        row_planes(r + dy, q);
+        load_planes(pl, ph, q);
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
           if (ring_dy(i) != dy) continue;
