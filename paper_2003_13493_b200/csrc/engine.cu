@@ -135,26 +135,6 @@ DeviceBatch::DeviceBatch(const DetectParams& p, int device, int width, int heigh
   check_cuda(cudaMemset(d_keys_, 0, sizeof(unsigned long long) * g_.cells * cap), "memset keys");
   check_cuda(cudaMemset(d_counts_, 0, sizeof(int) * cap), "memset counts");
   check_cuda(cudaMemset(d_stats_, 0, sizeof(uint64_t) * 2 * cap), "memset stats");
-  // In-cell key tables: for level k, column x -> cell_x << 10 | (1023 - (x - ox))
-  // with ox the first level-k column of that cell; rows likewise.
-  if (p_.cell_w <= 1024 && p_.cell_h <= 1024) {
-    std::vector<uint32_t> tab;
-    for (int k = 0; k < g_.levels; ++k) {
-      kt_col_[k] = static_cast<int>(tab.size());
-      for (int x = 0; x < g_.lw[k]; ++x) {
-        const int c = (x << k) / p_.cell_w, o = (c * p_.cell_w + (1 << k) - 1) >> k;
-        tab.push_back((static_cast<uint32_t>(c) << 10) | (1023u - static_cast<uint32_t>(x - o)));
-      }
-      kt_row_[k] = static_cast<int>(tab.size());
-      for (int y = 0; y < g_.lh[k]; ++y) {
-        const int c = (y << k) / p_.cell_h, o = (c * p_.cell_h + (1 << k) - 1) >> k;
-        tab.push_back((static_cast<uint32_t>(c) << 10) | (1023u - static_cast<uint32_t>(y - o)));
-      }
-    }
-    d_keytab_ = dalloc<uint32_t>(tab.size(), "key tables");
-    check_cuda(cudaMemcpy(d_keytab_, tab.data(), tab.size() * sizeof(uint32_t),
-                          cudaMemcpyHostToDevice), "upload key tables");
-  }
 }
 
 DeviceBatch::~DeviceBatch() {
@@ -169,7 +149,6 @@ DeviceBatch::~DeviceBatch() {
   cudaFree(d_stats_);
   cudaFree(d_naive_);
   cudaFree(d_conf_);
-  cudaFree(d_keytab_);
   if (cur >= 0) cudaSetDevice(cur);
 }
 
@@ -229,7 +208,8 @@ fused::Params fused_geometry(const DetectParams& p, const Geometry& g, int R, in
       static_cast<size_t>(std::max(fused::kOwn * (P.nw_max - 1) + 36, tw_max + 2 * n + 22)), 16));
   P.rp = static_cast<int>(round_up(static_cast<size_t>(tw_max + 4 * n), 8));
   // 32-bit in-cell keys need cells of at most 1024 px per side
-  P.key_slots = (p.cell_w <= 1024 && p.cell_h <= 1024 && slots <= 4096) ? slots : 0;
+  // 32-bit in-CTA keys (score << 20 | 10-bit y and x offsets inside the CTA)
+  P.key_slots = slots <= 4096 ? slots : 0;
   for (int i = 0; i < 32; ++i) P.pow2[i] = 1u << i;
   for (int b = 0; b < 8; ++b) P.emask[b] = ((p.epsilon >> b) & 1) ? 0xFFFFFFFFu : 0u;
   if (const char* e = std::getenv("FLKB_LIST_CAP")) P.list_cap = std::max(256, std::atoi(e));
@@ -383,12 +363,6 @@ void DeviceBatch::run(const uint8_t* frames, size_t fstride, int pitch, int coun
     if (k > 0 && k < 3) P.pyr_img[k] = pyr + g_.loff[k];
   }
   P.keys = keys;
-  P.keytab = d_keytab_;
-  if (!d_keytab_) P.key_slots = 0;  // cells wider than 1024 px: direct u64 atomics
-  for (int k = 0; k < g_.levels; ++k) {
-    P.lv[k].kt_col = kt_col_[k];
-    P.lv[k].kt_row = kt_row_[k];
-  }
   P.stats = stats ? st : nullptr;
   // detection of levels [kb, ke) in one launch
   auto detect = [&](int kb, int ke, int pyr_levels) {

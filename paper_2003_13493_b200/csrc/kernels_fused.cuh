@@ -22,8 +22,8 @@
 //  5. NMS   each candidate in the band's own rows is tested against its
 //           (2n+1)^2 window with spiral_is_local_max's tie rule
 //           (nms.cpp:48-79); survivors update a 32-bit per-cell key in
-//           shared memory with one ATOMS.MAX (score, -y, -x inside the cell;
-//           the level is fixed per CTA).
+//           shared memory with one ATOMS.MAX (score, -y, -x as offsets inside
+//           the CTA; the level is fixed per CTA).
 //  6. FLUSH each non-empty cell key becomes the global u64 key (score,
 //           -level, -y0, -x0) via one atomicMax -- the cross-level
 //           cell_candidate_wins order (nms.cpp:41-46).
@@ -76,7 +76,6 @@ struct Level {
   int tma;              // rows may be fetched with cp.async.bulk
   int nw;               // plane words per row (max over the level's tiles)
   FastDiv div_nw, div_tiles;
-  int kt_col, kt_row;   // offsets of this level's column / row key tables in keytab
 };
 
 struct Params {
@@ -97,9 +96,6 @@ struct Params {
   int list_cap;   // corner-list capacity override (0 = default 6144 entries)
   uint32_t pow2[32];  // 1 << i, read from the constant bank so shifts can issue as IMAD
   uint32_t emask[8];  // ~0 where bit b of eps is set
-  // In-cell key tables (DeviceBatch::keytab): per level, for every column x
-  // cell_x << 10 | (1023 - (x - first x of the cell)), then likewise per row.
-  const uint32_t* keytab;
   unsigned long long* keys;
   unsigned long long* stats;
 };
@@ -705,8 +701,8 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_detect(const __grid_co
     const int e_lo = T1 > T0 ? scan[kWarps + 1] : 0;
     const int e_hi = T1 > T0 ? scan[kWarps + 2] : 0;
     const int rp = P.rp;
-    const uint32_t* ktc = P.keytab + L.kt_col;  // this level's column / row key tables
-    const uint32_t* ktr = P.keytab + L.kt_row;
+    const uint32_t kc = static_cast<uint32_t>((1023 + y0) * 1024 + 1023 + x_lo);
+    const uint32_t pk = P.pow2[k];  // level -> level-0 coordinates
     for (int w0 = e_lo; w0 < e_hi; w0 += cap) {
       const bool resident = total <= cap;  // the scoring list is still in place
       const int off = resident ? 0 : w0;
@@ -768,12 +764,16 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_detect(const __grid_co
             if (!keep) continue;
           }
           if (local_keys) {
-            // in-cell key parts from the level's table: cell << 10 | (1023 - local)
-            const uint32_t ck = __ldg(ktc + static_cast<uint32_t>(x));
-            const uint32_t rk = __ldg(ktr + static_cast<uint32_t>(y));
-            const uint32_t key = (static_cast<uint32_t>(s) << 20) | ((rk & 1023u) << 10) | (ck & 1023u);
-            atomicMax(skeys + (static_cast<int>(rk >> 10) - cr0) * P.cols + static_cast<int>(ck >> 10),
-                      key);
+            // 32-bit key inside the CTA: score, then smaller y, then smaller x
+            // (the level is fixed per CTA), as s << 20 | (1023 - (y - y0)) << 10
+            // | (1023 - (x - x_lo)), built with IMADs; the cell from the
+            // level-0 coordinates with FastDivs (no table loads)
+            const uint32_t key = mad_fma(static_cast<uint32_t>(s), P.pow2[20],
+                                         kc - mad_fma(static_cast<uint32_t>(y), P.pow2[10],
+                                                      static_cast<uint32_t>(x)));
+            const int cx = P.div_cw(static_cast<int>(shl_fma(static_cast<uint32_t>(x), pk)));
+            const int cy = P.div_ch(static_cast<int>(shl_fma(static_cast<uint32_t>(y), pk)));
+            atomicMax(skeys + (cy - cr0) * P.cols + cx, key);
           } else {
             const int X = x << k, Y = y << k;
             atomicMax(P.keys + static_cast<size_t>(f) * P.cells + P.div_ch(Y) * P.cols + P.div_cw(X),
@@ -805,11 +805,8 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_detect(const __grid_co
   for (int i = tid; i < slots; i += kThreads) {
     const uint32_t key = skeys[i];
     if (!key) continue;
-    const int ccy = cr0 + i / P.cols, ccx = i % P.cols;
-    const int ox = (ccx * P.cell_w + (1 << k) - 1) >> k;
-    const int oy = (ccy * P.cell_h + (1 << k) - 1) >> k;
-    const int y = oy + 1023 - static_cast<int>((key >> 10) & 1023u);
-    const int x = ox + 1023 - static_cast<int>(key & 1023u);
+    const int y = y0 + 1023 - static_cast<int>((key >> 10) & 1023u);
+    const int x = x_lo + 1023 - static_cast<int>(key & 1023u);
     atomicMax(P.keys + static_cast<size_t>(f) * P.cells + i + cr0 * P.cols,
               pack_key(static_cast<int>(key >> 20), k, x << k, y << k));
   }
