@@ -223,6 +223,10 @@ def other_configs(device: int):
         del buf
         return fps
 
+    c1 = dict(epsilon=10, N=9, score_kind="mt", l=1, w=1, h=32, n=1)
+    fps = batch_fps(c1, 752, 480, 4096)
+    out["C1"] = {"workload": "752x480 l=1 FAST-9 mt (threshold score), 32x32 cells, batch 4096, "
+                             "S2 frames on device", "frames_per_s": fps, "mpix_per_s": fps * 752 * 480 / 1e6}
     c3 = dict(epsilon=10, N=12, score_kind="sad_b", l=4, w=1, h=2, n=1)
     fps = batch_fps(c3, 1920, 1080, 256, cell=(16, 16))
     out["C3"] = {"workload": "1920x1080 l=4 FAST-12 sad_b, 16x16 cells (extension), batch 256, "
