@@ -191,13 +191,15 @@ __global__ void __launch_bounds__(256) k_template(Levels lv, const int* __restri
 // residual and its products with the coefficients, one thread per parameter
 // sums them in pixel order, and every thread then applies the identical
 // update (deterministic, no broadcast needed).
-__global__ void __launch_bounds__(256) k_track(Levels lv, TrackIO* __restrict__ io,
+__global__ void __launch_bounds__(256) k_track(Levels lv, const int* __restrict__ n_tracks,
+                                               TrackIO* __restrict__ io,
                                                const TplLevel* __restrict__ hdr,
                                                const float* __restrict__ vals,
                                                const double* __restrict__ coef, TrackerParams tp) {
   __shared__ double prod[4][kMaxPx];
   __shared__ double rhs[4];
   const int t = blockIdx.x, tid = threadIdx.x, L = lv.n;
+  if (t >= *n_tracks) return;  // the frame graph launches one CTA per slot
   const int slot = io[t].slot;
   double tx0 = io[t].w[0], ty0 = io[t].w[1], gain = io[t].w[2], offset = io[t].w[3];
   int iters = 0, status = 0;
@@ -331,6 +333,8 @@ Session::~Session() {
   cudaFree(d_coef_);
   cudaFree(d_io_);
   cudaFreeHost(h_io_);
+  for (auto ge : graph_exec_)
+    if (ge) cudaGraphExecDestroy(ge);
   for (auto e : ev_)
     if (e) cudaEventDestroy(e);
   if (stream_) cudaStreamDestroy(stream_);
@@ -362,13 +366,70 @@ void Session::setup(int width, int height) {
   check_cuda(cudaMalloc(&d_hdr_, per * sizeof(lk::TplLevel)), "templates");
   check_cuda(cudaMalloc(&d_vals_, per * lk::kMaxPx * sizeof(float)), "templates");
   check_cuda(cudaMalloc(&d_coef_, per * lk::kMaxPx * 4 * sizeof(double)), "templates");
-  io_bytes_ = std::max(static_cast<size_t>(slots_) * sizeof(lk::TrackIO),
-                       static_cast<size_t>(slots_) * 3 * sizeof(int) + per * sizeof(int));
+  io_bytes_ = kIoHeader + std::max(static_cast<size_t>(slots_) * sizeof(lk::TrackIO),
+                                   static_cast<size_t>(slots_) * 3 * sizeof(int) + per * sizeof(int));
   check_cuda(cudaMalloc(&d_io_, io_bytes_), "session io");
   check_cuda(cudaMallocHost(&h_io_, io_bytes_), "session io (pinned)");
   free_.clear();
   for (int s = slots_ - 1; s >= 0; --s) free_.push_back(s);
   tracks_.clear();
+  capture_frame_graph();
+}
+
+// The per-frame GPU work as one CUDA graph (replayed with one launch):
+// H2D frame -> pyramid -> H2D track records (count in the header) -> k_track
+// over every slot (CTAs past the live count exit) -> D2H records, with the
+// stage events inside. Shapes and pointers are fixed per session.
+void Session::capture_frame_graph() {
+  for (int timed = 0; timed < 2; ++timed) {
+    if (graph_exec_[timed]) cudaGraphExecDestroy(graph_exec_[timed]);
+    graph_exec_[timed] = nullptr;
+  }
+  const Geometry& g = batch_->geometry();
+  lk::Levels lv{};
+  lv.n = g.levels;
+  for (int k = 0; k < g.levels; ++k) {
+    lv.img[k] = k == 0 ? d_frame_ : batch_->device_pyramid() + g.loff[k];
+    lv.pitch[k] = k == 0 ? pitch_ : g.lpitch[k];
+    lv.w[k] = g.lw[k];
+    lv.h[k] = g.lh[k];
+  }
+  const size_t frame_bytes = static_cast<size_t>(pitch_) * g.height;
+  const size_t io_bytes = kIoHeader + sizeof(lk::TrackIO) * static_cast<size_t>(slots_);
+  // two variants: plain, and with stage events (external event-record nodes
+  // cost the replay ~20 us, so they are only in the graph used for stats)
+  for (int timed = 0; timed < 2; ++timed) {
+    auto mark = [&](int i) {
+      if (timed)
+        check_cuda(cudaEventRecordWithFlags(ev_[i], stream_, cudaEventRecordExternal), "event");
+    };
+    cudaGraph_t graph = nullptr;
+    check_cuda(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal), "capture");
+    try {
+      mark(0);
+      check_cuda(cudaMemcpyAsync(d_frame_, h_frame_, frame_bytes, cudaMemcpyHostToDevice, stream_),
+                 "H2D frame");
+      graph_launches_ = batch_->enqueue_pyramid(d_frame_, frame_bytes, pitch_, 1, stream_, 0);
+      mark(1);
+      check_cuda(cudaMemcpyAsync(d_io_, h_io_, io_bytes, cudaMemcpyHostToDevice, stream_),
+                 "H2D tracks");
+      lk::k_track<<<slots_, 256, 0, stream_>>>(lv, reinterpret_cast<const int*>(d_io_),
+                                               reinterpret_cast<lk::TrackIO*>(d_io_ + kIoHeader),
+                                               d_hdr_, d_vals_, d_coef_, tp_);
+      ++graph_launches_;
+      check_cuda(cudaMemcpyAsync(h_io_, d_io_, io_bytes, cudaMemcpyDeviceToHost, stream_),
+                 "D2H tracks");
+      mark(2);
+    } catch (...) {
+      cudaStreamEndCapture(stream_, &graph);
+      if (graph) cudaGraphDestroy(graph);
+      throw;
+    }
+    check_cuda(cudaStreamEndCapture(stream_, &graph), "end capture");
+    const cudaError_t e = cudaGraphInstantiate(&graph_exec_[timed], graph, 0);
+    cudaGraphDestroy(graph);
+    check_cuda(e, "graph instantiate");
+  }
 }
 
 void Session::process(const HostImage& img, std::vector<flk_track_info>* out,
@@ -410,11 +471,15 @@ void Session::process(const HostImage& img, std::vector<flk_track_info>* out,
     std::memcpy(h_frame_ + static_cast<size_t>(y) * pitch_,
                 img.px.data() + static_cast<size_t>(y) * img.width, img.width);
   const auto tt1 = Clock::now();
-  check_cuda(cudaEventRecord(ev_[0], stream_), "event");
-  check_cuda(cudaMemcpyAsync(d_frame_, h_frame_, static_cast<size_t>(pitch_) * img.height,
-                             cudaMemcpyHostToDevice, stream_), "H2D frame");
-  batch_->build_pyramid(d_frame_, static_cast<size_t>(pitch_) * img.height, pitch_, 1, stream_);
-  check_cuda(cudaEventRecord(ev_[1], stream_), "event");
+  const int n = static_cast<int>(tracks_.size());
+  *reinterpret_cast<int*>(h_io_) = n;
+  lk::TrackIO* io = reinterpret_cast<lk::TrackIO*>(h_io_ + kIoHeader);
+  for (int i = 0; i < n; ++i) {
+    std::copy(tracks_[i].warp, tracks_[i].warp + 4, io[i].w);
+    io[i].slot = tracks_[i].slot;
+  }
+  check_cuda(cudaGraphLaunch(graph_exec_[stats ? 1 : 0], stream_), "frame graph");
+  count_launches(graph_launches_);
   lk::Levels lv{};
   lv.n = L;
   for (int k = 0; k < L; ++k) {
@@ -423,38 +488,19 @@ void Session::process(const HostImage& img, std::vector<flk_track_info>* out,
     lv.w[k] = g.lw[k];
     lv.h[k] = g.lh[k];
   }
-  const int n = static_cast<int>(tracks_.size());
-  lk::TrackIO* io = reinterpret_cast<lk::TrackIO*>(h_io_);
-  if (n > 0) {
-    for (int i = 0; i < n; ++i) {
-      std::copy(tracks_[i].warp, tracks_[i].warp + 4, io[i].w);
-      io[i].slot = tracks_[i].slot;
-    }
-    const size_t bytes = sizeof(lk::TrackIO) * n;
-    check_cuda(cudaMemcpyAsync(d_io_, h_io_, bytes, cudaMemcpyHostToDevice, stream_), "H2D tracks");
-    lk::k_track<<<n, 256, 0, stream_>>>(lv, reinterpret_cast<lk::TrackIO*>(d_io_), d_hdr_, d_vals_,
-                                        d_coef_, tp_);
-    check_cuda(cudaGetLastError(), "k_track");
-    count_launches(1);
-    check_cuda(cudaMemcpyAsync(h_io_, d_io_, bytes, cudaMemcpyDeviceToHost, stream_), "D2H tracks");
-  }
-  check_cuda(cudaEventRecord(ev_[2], stream_), "event");
   const auto tt2 = Clock::now();
   check_cuda(cudaStreamSynchronize(stream_), "pyramid + track");
-  if (trace) {
-    float a = 0, b = 0;
-    cudaEventElapsedTime(&a, ev_[0], ev_[1]);
-    cudaEventElapsedTime(&b, ev_[1], ev_[2]);
-    std::fprintf(stderr, "flkb session: memcpy %.1f submit %.1f wait %.1f | dev pyr %.1f trk %.1f us\n",
+  if (trace)
+    std::fprintf(stderr, "flkb session: memcpy %.1f submit %.1f wait %.1f us\n",
                  std::chrono::duration<double, std::micro>(tt1 - tt0).count(),
-                 std::chrono::duration<double, std::micro>(tt2 - tt1).count(), us_since(tt2),
-                 a * 1e3, b * 1e3);
+                 std::chrono::duration<double, std::micro>(tt2 - tt1).count(), us_since(tt2));
+  if (stats) {
+    float ms_pyr = 0, ms_trk = 0;
+    check_cuda(cudaEventElapsedTime(&ms_pyr, ev_[0], ev_[1]), "stage time");
+    check_cuda(cudaEventElapsedTime(&ms_trk, ev_[1], ev_[2]), "stage time");
+    st.pyramid_us = ms_pyr * 1e3;
+    st.track_us = ms_trk * 1e3;
   }
-  float ms_pyr = 0, ms_trk = 0;
-  cudaEventElapsedTime(&ms_pyr, ev_[0], ev_[1]);
-  cudaEventElapsedTime(&ms_trk, ev_[1], ev_[2]);
-  st.pyramid_us = ms_pyr * 1e3;
-  st.track_us = ms_trk * 1e3;
 
   // advance live tracks (frontend.cpp:100-131)
   std::vector<flk_track_info> retired;

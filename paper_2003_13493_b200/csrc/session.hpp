@@ -67,6 +67,8 @@ class Session {
     int birth_frame;
   };
   void setup(int width, int height);
+  void capture_frame_graph();
+  static constexpr size_t kIoHeader = 64;  // live-track count ahead of the TrackIO records
 
   Config cfg_;
   DetectParams p_;
@@ -75,6 +77,8 @@ class Session {
   std::unique_ptr<DeviceBatch> batch_;
   cudaStream_t stream_ = nullptr;
   cudaEvent_t ev_[3] = {nullptr, nullptr, nullptr};
+  cudaGraphExec_t graph_exec_[2] = {nullptr, nullptr};  // plain, with stage events
+  int graph_launches_ = 0;
   uint8_t* d_frame_ = nullptr;
   uint8_t* h_frame_ = nullptr;  // pinned staging
   int pitch_ = 0;
