@@ -198,6 +198,7 @@ __global__ void __launch_bounds__(256) k_track(Levels lv, const int* __restrict_
                                                const double* __restrict__ coef, TrackerParams tp) {
   __shared__ double prod[4][kMaxPx];
   __shared__ double rhs[4];
+  __shared__ double hinv_s[16];
   const int t = blockIdx.x, tid = threadIdx.x, L = lv.n;
   if (t >= *n_tracks) return;  // the frame graph launches one CTA per slot
   const int slot = io[t].slot;
@@ -219,6 +220,11 @@ __global__ void __launch_bounds__(256) k_track(Levels lv, const int* __restrict_
     const double ax = T.ax, ay = T.ay;
     const double max_step = 0.5 * hypot(static_cast<double>(w), static_cast<double>(h));
     const size_t base = (static_cast<size_t>(slot) * L + k) * kMaxPx;
+    // the level's inverse Hessian in shared memory (read by every thread for
+    // the identical update each iteration)
+    __syncthreads();  // the previous level's last update has read hinv_s
+    if (tid < 16) hinv_s[tid] = T.hinv[tid];
+    __syncthreads();
     // this thread's template pixel, fixed for the level: kept in registers
     const int oy = -half + tid / patch, ox = -half + tid % patch;
     double tv = 0.0, u[4] = {0.0, 0.0, 0.0, 0.0};
@@ -252,7 +258,7 @@ __global__ void __launch_bounds__(256) k_track(Levels lv, const int* __restrict_
       double delta[4] = {0.0, 0.0, 0.0, 0.0};
       for (int r = 0; r < dims; ++r) {
         double acc = 0.0;
-        for (int c = 0; c < dims; ++c) acc += T.hinv[r * dims + c] * rhs[c];
+        for (int c = 0; c < dims; ++c) acc += hinv_s[r * dims + c] * rhs[c];
         delta[r] = acc;
       }
       ++iters;
