@@ -133,6 +133,12 @@ DeviceBatch::DeviceBatch(const DetectParams& p, int device, int width, int heigh
   d_counts_ = dalloc<int>(cap, "counts");
   d_stats_ = dalloc<uint64_t>(2 * cap, "stats");
   check_cuda(cudaMemset(d_keys_, 0, sizeof(unsigned long long) * g_.cells * cap), "memset keys");
+  // the staged score maps' pitch padding is never written: zeroed once so a
+  // whole-map download reads defined bytes
+  check_cuda(cudaMemset(d_resp_, 0, sizeof(uint16_t) * resp_frame_elems_ * cap), "memset responses");
+  // feature slots past a frame's count are never written; the batch download
+  // copies whole frame slots
+  check_cuda(cudaMemset(d_feats_, 0, sizeof(flk_feature) * g_.cells * cap), "memset features");
   check_cuda(cudaMemset(d_counts_, 0, sizeof(int) * cap), "memset counts");
   check_cuda(cudaMemset(d_stats_, 0, sizeof(uint64_t) * 2 * cap), "memset stats");
 }

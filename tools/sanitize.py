@@ -1,0 +1,56 @@
+#!/usr/bin/env python
+"""Small representative runs for compute-sanitizer (memcheck / racecheck /
+synccheck / initcheck): the fused detector (both pyramid plans, radius 1-3,
+every score kind, unaligned pitch, multi-round corner lists), the staged
+kernels, the conformance kernel and a short tracking session. Checks parity
+with the oracle on each so a sanitizer run is also a correctness run.
+
+    compute-sanitizer --tool racecheck python tools/sanitize.py
+"""
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path[:0] = [ROOT, os.path.join(ROOT, "tests")]
+
+import numpy as np  # noqa: E402
+
+import oracle  # noqa: E402
+import paper_2003_13493_b200 as fl  # noqa: E402
+import sessions  # noqa: E402
+import synth  # noqa: E402
+
+
+def main():
+    orc = oracle.load_oracle()
+    cases = [
+        (synth.texture(1, 256, 160), dict(epsilon=10, N=9, score_kind="sad_b", l=3, w=1, h=8, n=1), "1"),
+        (synth.noise(2, 200, 120), dict(epsilon=10, N=12, score_kind="mt", l=2, w=1, h=16, n=2), "0"),
+        (synth.texture(3, 193, 97), dict(epsilon=5, N=10, score_kind="sad_a", l=2, w=2, h=4, n=3), "1"),
+        (synth.noise(4, 160, 96), dict(epsilon=0, N=9, score_kind="sad_b", l=1, w=1, h=32, n=1), "0"),
+    ]
+    for img, cfg, fuse in cases:
+        os.environ["FLKB_FUSE_PYR"] = fuse
+        det = fl.Detector(fl.Config(**cfg))
+        feats, extra = det.run(img, stats=True, conformance=True)
+        ref, st = orc.detect(img, oracle.make_params(**cfg))
+        assert (feats == ref).all() and extra["stats"]["nms_comparisons"] == st.comparisons
+        assert (det.run(img) == ref).all()
+        maps = det.responses(img, cfg["l"])
+        for a, b in zip(maps, orc.responses(img, oracle.make_params(**cfg))):
+            assert (a == b).all()
+    os.environ["FLKB_LIST_CAP"] = "256"  # multi-round corner lists
+    img = synth.noise(5, 200, 120)
+    cfg = dict(epsilon=0, N=9, score_kind="sad_b", l=2, w=1, h=16, n=1)
+    feats = fl.Detector(fl.Config(**cfg)).run(img)
+    assert (feats == orc.detect(img, oracle.make_params(**cfg))[0]).all()
+    del os.environ["FLKB_LIST_CAP"]
+    frames = sessions.drifting_sequence(3, 192, 128)
+    scfg = dict(epsilon=10, N=9, score_kind="sad_b", l=2, w=1, h=16, n=1, target_count=12,
+                redetect_ratio=0.5, param_mode="full", max_iterations=30, convergence_epsilon=0.01)
+    sessions.run_capi_session(fl.load_library(), scfg, frames)
+    print("sanitize driver ok")
+
+
+if __name__ == "__main__":
+    main()
