@@ -41,6 +41,8 @@ W, H, LEVELS = 752, 480, 3
 PITCH = 768
 CFG = dict(epsilon=10, N=9, score_kind="sad_b", l=3, w=1, h=8, n=1)
 METRIC = json.load(open(os.path.join(ROOT, "BASELINE.json")))["metric"]
+WORKLOAD = ("C4: 752x480, l=3, FAST-9 sad_b eps=10, 32x32 cells (w=1,h=8), n=1; "
+            "BASELINE configs[3]")
 
 
 def level_pixels():
@@ -363,7 +365,7 @@ def run_reference_arm(args, rank: int, world: int):
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
             "data": "synthetic (S2 texture)", "impl": "reference",
             "mpix_per_s": fps * W * H / 1e6,
-            "config": {"workload": "C4 752x480 l=3 FAST-9 sad_b eps=10 32x32 cells n=1",
+            "config": {"workload": WORKLOAD,
                        "frames_per_step": per_step, "parallelism": f"{workers} host threads"},
             "cpu_baseline": {"value": fps, "unit": "frames/s", "cores": workers,
                              "kind": "reference",
@@ -501,8 +503,7 @@ def main():
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
             "data": "synthetic (S2 counter-hash texture generated on device, SURVEY 8d)",
             "mpix_per_s": fps * W * H / 1e6,
-            "config": {"workload": "C4: 752x480, l=3, FAST-9 sad_b eps=10, 32x32 cells (w=1,h=8), "
-                                   "n=1; BASELINE configs[3]",
+            "config": {"workload": WORKLOAD,
                        "frames_per_gpu_per_step": B, "global_frames_per_step": B * world,
                        "parallelism": f"frame shards x{world}, no collective",
                        "l2": f"inputs {B * W * H / 1e9:.2f} GB/GPU > 126 MB L2 (no flush needed)"},
