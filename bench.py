@@ -283,6 +283,23 @@ def session_line(device: int):
 
     run_sequence()  # warm-up (allocations, module load)
     ts, live = run_sequence()
+
+    def run_many(k):  # k sessions advanced together (flkb_sessions_process)
+        ss = [fl.Session(fl.Config(**SESSION_CFG)) for _ in range(k)]
+        sh = (ctypes.c_void_p * k)(*[x.handle.value for x in ss])
+        outs = (ctypes.c_void_p * k)()
+        t0 = time.perf_counter()
+        for im in imgs:
+            ih = (ctypes.c_void_p * k)(*([im.handle.value] * k))
+            assert lib.flkb_sessions_process(sh, ih, k, outs, None) == 0
+            for i in range(k):
+                lib.flk_tracks_destroy(ctypes.c_void_p(outs[i]))
+        return k * len(imgs) / (time.perf_counter() - t0)
+
+    many = {}
+    for k in (1, 4, 8, 16):
+        run_many(k)
+        many[k] = run_many(k)
     cold, ts = ts[0] / 1e6, ts[1:]
     parts = []
     s3 = fl.Session(fl.Config(**SESSION_CFG))
@@ -300,6 +317,7 @@ def session_line(device: int):
             "stage_us_median": {"pyramid": float(np.median(parts[:, 0])),
                                 "track": float(np.median(parts[:, 1]))},
             "lk_iterations_per_track": float(parts[:, 3].sum() / max(1, parts[:, 2].sum())),
+            "concurrent_sessions_frames_per_s": {str(k): v for k, v in many.items()},
             "includes": "H2D of the frame, pyramid, LK kernel over every live track, D2H of "
                         "warps, host lifecycle; re-detection + template kernels when fired"}
 

@@ -99,6 +99,20 @@ FLK_API flk_status flkb_synth_frames_device(uint8_t* frames, int kind, uint64_t 
 FLK_API flk_status flkb_detector_responses(flk_detector* detector, const flk_image* image,
                                            float* out);
 
+/* ------------------------------------------------------- many sessions */
+
+/* Advances n independent tracking sessions by one frame each, overlapping
+ * their GPU work: every session's frame is staged and its frame graph
+ * (pyramid + LK) enqueued on the session's own stream first, then each is
+ * completed in order (re-detection frames run their detector inside the
+ * completion). Per session the result is exactly flk_session_process's;
+ * out_tracks[i] receives session i's snapshot (caller frees each) and stats
+ * may be NULL or an array of n. On an error the sessions already submitted
+ * are still completed and returned; the others get NULL. */
+FLK_API flk_status flkb_sessions_process(flk_session* const* sessions,
+                                         const flk_image* const* images, int n,
+                                         flk_tracks** out_tracks, flk_frame_stats* stats);
+
 /* Number of CUDA kernels this library has launched in the process (graph
  * replays count every kernel node). */
 FLK_API uint64_t flkb_kernel_launch_count(void);

@@ -422,6 +422,49 @@ flk_status flk_session_process(flk_session* session, const flk_image* image,
 
 void flk_session_destroy(flk_session* session) { delete session; }
 
+flk_status flkb_sessions_process(flk_session* const* sessions, const flk_image* const* images,
+                                 int n, flk_tracks** out_tracks, flk_frame_stats* stats) {
+  if (!sessions || !images || !out_tracks || n < 0)
+    return fail(FLK_E_INVALID_ARG, "sessions, images, and out_tracks must not be NULL");
+  for (int i = 0; i < n; ++i) {
+    out_tracks[i] = nullptr;
+    if (!sessions[i] || !images[i]) return fail(FLK_E_INVALID_ARG, "NULL session or image");
+  }
+  int submitted = 0;
+  flk_status first = FLK_OK;
+  std::string first_msg;
+  // submit every frame first so the sessions' graphs overlap on the GPU
+  for (; submitted < n; ++submitted) {
+    const flk_status st = guarded([&] {
+      sessions[submitted]->session->submit(images[submitted]->img, stats != nullptr);
+      return FLK_OK;
+    });
+    if (st != FLK_OK) {
+      first = st;
+      first_msg = g_error;
+      break;
+    }
+  }
+  for (int i = 0; i < submitted; ++i) {
+    const flk_status st = guarded([&] {
+      auto t = std::make_unique<flk_tracks>();
+      sessions[i]->session->complete(images[i]->img, &t->items, stats ? stats + i : nullptr,
+                                     nullptr);
+      out_tracks[i] = t.release();
+      return FLK_OK;
+    });
+    if (st != FLK_OK && first == FLK_OK) {
+      first = st;
+      first_msg = g_error;
+    }
+  }
+  if (first != FLK_OK) return fail(first, first_msg.c_str());
+  g_error.clear();
+  return FLK_OK;
+}
+
+
+
 int flk_tracks_count(const flk_tracks* tracks) {
   return tracks ? static_cast<int>(tracks->items.size()) : 0;
 }

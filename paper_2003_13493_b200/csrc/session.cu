@@ -440,6 +440,13 @@ void Session::capture_frame_graph() {
 
 void Session::process(const HostImage& img, std::vector<flk_track_info>* out,
                       flk_frame_stats* stats, flk_conformance* conformance) {
+  submit(img, stats != nullptr);
+  complete(img, out, stats, conformance);
+}
+
+// First half of a frame: validation, staging and the frame graph (pyramid +
+// LK over the live tracks) enqueued on the session's stream; no host wait.
+void Session::submit(const HostImage& img, bool timed) {
   const int cw = cfg_.cell_width(), ch = cfg_.cell_height();
   const int cols = (img.width + cw - 1) / cw, rows = (img.height + ch - 1) / ch;
   if (frame_index_ == 0) {
@@ -484,8 +491,26 @@ void Session::process(const HostImage& img, std::vector<flk_track_info>* out,
     std::copy(tracks_[i].warp, tracks_[i].warp + 4, io[i].w);
     io[i].slot = tracks_[i].slot;
   }
-  check_cuda(cudaGraphLaunch(graph_exec_[stats ? 1 : 0], stream_), "frame graph");
+  check_cuda(cudaGraphLaunch(graph_exec_[timed ? 1 : 0], stream_), "frame graph");
   count_launches(graph_launches_);
+  submitted_ = true;
+  t_submit_ = std::chrono::duration<double, std::micro>(tt1 - tt0).count();
+}
+
+// Second half: wait for the frame graph, then the lifecycle of
+// frontend.cpp:100-225 (retire, trigger, re-detection, dedupe, spawn, output).
+void Session::complete(const HostImage& img, std::vector<flk_track_info>* out,
+                       flk_frame_stats* stats, flk_conformance* conformance) {
+  if (!submitted_) throw InvalidArgument("no submitted frame to complete");
+  submitted_ = false;
+  static const bool trace = std::getenv("FLKB_SESSION_TRACE") != nullptr;
+  DeviceGuard guard(device_);
+  const int cw = cfg_.cell_width(), ch = cfg_.cell_height();
+  const Geometry& g = batch_->geometry();
+  const int L = g.levels;
+  flk_frame_stats st{};
+  const int n = static_cast<int>(tracks_.size());
+  lk::TrackIO* io = reinterpret_cast<lk::TrackIO*>(h_io_ + kIoHeader);
   lk::Levels lv{};
   lv.n = L;
   for (int k = 0; k < L; ++k) {
@@ -497,9 +522,7 @@ void Session::process(const HostImage& img, std::vector<flk_track_info>* out,
   const auto tt2 = Clock::now();
   check_cuda(cudaStreamSynchronize(stream_), "pyramid + track");
   if (trace)
-    std::fprintf(stderr, "flkb session: memcpy %.1f submit %.1f wait %.1f us\n",
-                 std::chrono::duration<double, std::micro>(tt1 - tt0).count(),
-                 std::chrono::duration<double, std::micro>(tt2 - tt1).count(), us_since(tt2));
+    std::fprintf(stderr, "flkb session: staging %.1f us, wait %.1f us\n", t_submit_, us_since(tt2));
   if (stats) {
     float ms_pyr = 0, ms_trk = 0;
     check_cuda(cudaEventElapsedTime(&ms_pyr, ev_[0], ev_[1]), "stage time");

@@ -57,6 +57,13 @@ class Session {
 
   void process(const HostImage& img, std::vector<flk_track_info>* out, flk_frame_stats* stats,
                flk_conformance* conformance);
+  // process() in two halves, so several sessions can overlap on the GPU:
+  // submit() stages the frame and enqueues its graph on the session's
+  // stream; complete() waits for it and runs the lifecycle (and any
+  // re-detection) for the same image.
+  void submit(const HostImage& img, bool timed);
+  void complete(const HostImage& img, std::vector<flk_track_info>* out, flk_frame_stats* stats,
+                flk_conformance* conformance);
 
  private:
   struct Track {
@@ -79,6 +86,8 @@ class Session {
   cudaEvent_t ev_[3] = {nullptr, nullptr, nullptr};
   cudaGraphExec_t graph_exec_[2] = {nullptr, nullptr};  // plain, with stage events
   int graph_launches_ = 0;
+  bool submitted_ = false;
+  double t_submit_ = 0;
   uint8_t* d_frame_ = nullptr;
   uint8_t* h_frame_ = nullptr;  // pinned staging
   int pitch_ = 0;

@@ -102,7 +102,8 @@ EXT_SYMBOLS = [
     "flkb_batch_run_host", "flkb_batch_download", "flkb_batch_frame_capacity",
     "flkb_batch_device_counts", "flkb_batch_device_features", "flkb_batch_device_stats",
     "flkb_batch_device_pyramid", "flkb_synth_frames_device", "flkb_kernel_launch_count",
-    "flkb_batch_kernels_per_run", "flkb_detector_responses", "flkb_batch_run_device_timed"]
+    "flkb_batch_kernels_per_run", "flkb_detector_responses", "flkb_batch_run_device_timed",
+    "flkb_sessions_process"]
 
 _lib = None
 _vp = ctypes.c_void_p
@@ -174,6 +175,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.flk_tracks_count.argtypes = [_vp]
     lib.flk_tracks_get.argtypes = [_vp, ctypes.c_int, _vp]
     lib.flk_track_status_name.argtypes = [ctypes.c_int]
+    lib.flkb_sessions_process.argtypes = [_vp, _vp, ctypes.c_int, _vp, _vp]
     lib.flkb_synth_frames_device.argtypes = [_vp, ctypes.c_int, ctypes.c_uint64, ctypes.c_int,
                                              ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                              ctypes.c_size_t, _vp]
@@ -330,6 +332,29 @@ class Session(_Handle):
         if cf is not None:
             extra["conformance"] = {k: getattr(cf, k) for k, _ in ConformanceT._fields_}
         return (out, extra) if extra else out
+
+
+def sessions_process(sessions, images):
+    """flkb_sessions_process: one frame for each session, GPU work overlapped.
+    Returns the per-session TRACK_DTYPE arrays (as Session.process)."""
+    n = len(sessions)
+    imgs = [Image.from_array(i) if isinstance(i, np.ndarray) else i for i in images]
+    sh = (_vp * n)(*[s.handle.value for s in sessions])
+    ih = (_vp * n)(*[i.handle.value for i in imgs])
+    outs = (_vp * n)()
+    _check(_lib.flkb_sessions_process(sh, ih, n, outs, None))
+    res = []
+    for i in range(n):
+        th = _vp(outs[i])
+        try:
+            m = _lib.flk_tracks_count(th)
+            out = np.zeros(m, TRACK_DTYPE)
+            for j in range(m):
+                _check(_lib.flk_tracks_get(th, j, out[j:].ctypes.data))
+        finally:
+            _lib.flk_tracks_destroy(th)
+        res.append(out)
+    return res
 
 
 class Detector(_Handle):

@@ -114,3 +114,47 @@ def test_session_launches_kernels():
     res = sessions.run_capi_session(fl.load_library(), cfg, frames)
     assert fl.kernel_launch_count() - before >= 3 * 2
     assert res[1][1]["tracks_entering"] > 0
+
+
+def test_many_sessions_overlapped_match_golden(gold):
+    """flkb_sessions_process: several independent sessions (different sizes,
+    configs and sequences) advanced together; each session's tracks and
+    counters are its golden digest, as if it ran alone."""
+    cases = [c for c in SESSIONS if c[0] in ("slide_512x256_l2", "drift_320x240_l3_full",
+                                             "drift_translation", "slide_maxit2", "noise_l3_n2")]
+    seqs = {name: sessions.sequence(kind, n, w, h) for name, kind, n, w, h, _ in cases}
+    sess = {name: fl.Session(fl.Config(**cfg)) for name, _, _, _, _, cfg in cases}
+    got = {name: [] for name in seqs}
+    lib = fl.load_library()
+    import ctypes
+    from sessions import FrameStats
+    for f in range(max(len(v) for v in seqs.values())):
+        live = [name for name in seqs if f < len(seqs[name])]
+        imgs = [fl.Image.from_array(seqs[name][f]) for name in live]
+        sh = (ctypes.c_void_p * len(live))(*[sess[name].handle.value for name in live])
+        ih = (ctypes.c_void_p * len(live))(*[i.handle.value for i in imgs])
+        outs = (ctypes.c_void_p * len(live))()
+        st = (FrameStats * len(live))()
+        assert lib.flkb_sessions_process(sh, ih, len(live), outs, st) == 0
+        for i, name in enumerate(live):
+            th = ctypes.c_void_p(outs[i])
+            m = lib.flk_tracks_count(th)
+            arr = np.zeros(m, sessions.TRACK_DTYPE)
+            for j in range(m):
+                assert lib.flk_tracks_get(th, j, arr[j:].ctypes.data) == 0
+            lib.flk_tracks_destroy(th)
+            got[name].append((arr, st[i].counters()))
+    for name in seqs:
+        assert sessions.digest(got[name]) == gold[name]["frames"], name
+
+
+def test_many_sessions_python_wrapper():
+    name, kind, n, w, h, cfg = SESSIONS[2]
+    frames = sessions.sequence(kind, n, w, h)
+    a, b = fl.Session(fl.Config(**cfg)), fl.Session(fl.Config(**cfg))
+    solo = fl.Session(fl.Config(**cfg))
+    for f in frames:
+        ra, rb = fl.sessions_process([a, b], [f, f])
+        rs = solo.process(f)
+        for k in sessions.RECORD_FIELDS:
+            assert (ra[k] == rs[k]).all() and (rb[k] == rs[k]).all()
