@@ -99,7 +99,7 @@ class FrameRunner {
   void run(const flkb::HostImage& img, std::vector<flk_feature>* feats, flk_frame_stats* stats,
            flk_conformance* conf) {
     flkb::DeviceGuard guard(device_);
-    stage(img);
+    copy_in(img);
     int* counts = static_cast<int*>(out_.p);
     flk_feature* fv = reinterpret_cast<flk_feature*>(static_cast<char*>(out_.p) + 4 * sizeof(int));
     const int cells = batch_.geometry().cells;
@@ -109,7 +109,6 @@ class FrameRunner {
       flkb::check_cuda(cudaGraphLaunch(exec_, stream_), "cudaGraphLaunch");
       flkb::count_launches(batch_.kernels_per_run());
     } else {
-      enqueue_copy_in();
       flkb::StageTimes t;
       batch_.run(d_in_, static_cast<size_t>(pitch_) * h_, pitch_, 1, true, stream_, &t);
       batch_.download(0, 1, counts, fv, stream_);
@@ -137,31 +136,32 @@ class FrameRunner {
   // Staged run that keeps the score maps, for flkb_detector_responses.
   void responses(const flkb::HostImage& img, float* out) {
     flkb::DeviceGuard guard(device_);
-    stage(img);
-    enqueue_copy_in();
+    copy_in(img);
     batch_.run_staged(d_in_, static_cast<size_t>(pitch_) * h_, pitch_, 1, false, stream_);
     batch_.download_responses(0, out, stream_);
   }
 
  private:
-  // The staging buffer holds the frame at the device pitch: one contiguous
-  // DMA (a pitched 2-D copy of a small frame takes the copy engine far longer).
-  void enqueue_copy_in() {
-    flkb::check_cuda(cudaMemcpyAsync(d_in_, in_.p, static_cast<size_t>(pitch_) * h_,
+  // One contiguous DMA of the frame at the device pitch (a pitched 2-D copy
+  // of a small frame takes the copy engine far longer): straight from the
+  // image's page-locked pixels when its rows already have the device pitch,
+  // else through the pinned staging buffer.
+  void copy_in(const flkb::HostImage& img) {
+    const uint8_t* src = img.px.data();
+    if (!(pitch_ == w_ && img.pinned())) {
+      uint8_t* dst = static_cast<uint8_t*>(in_.p);
+      for (int y = 0; y < h_; ++y)
+        std::memcpy(dst + static_cast<size_t>(y) * pitch_, src + static_cast<size_t>(y) * w_, w_);
+      src = dst;
+    }
+    flkb::check_cuda(cudaMemcpyAsync(d_in_, src, static_cast<size_t>(pitch_) * h_,
                                      cudaMemcpyHostToDevice, stream_), "H2D frame");
-  }
-  void stage(const flkb::HostImage& img) {
-    uint8_t* dst = static_cast<uint8_t*>(in_.p);
-    for (int y = 0; y < h_; ++y)
-      std::memcpy(dst + static_cast<size_t>(y) * pitch_, img.px.data() + static_cast<size_t>(y) * w_,
-                  w_);
   }
   void capture() {
     int* counts = static_cast<int*>(out_.p);
     flk_feature* fv = reinterpret_cast<flk_feature*>(static_cast<char*>(out_.p) + 4 * sizeof(int));
     flkb::check_cuda(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal), "capture");
-    try {
-      enqueue_copy_in();
+    try {  // the frame's H2D precedes each replay (its source may change)
       batch_.run(d_in_, static_cast<size_t>(pitch_) * h_, pitch_, 1, false, stream_);
       batch_.download(0, 1, counts, fv, stream_);
     } catch (...) {

@@ -62,11 +62,34 @@ void validate(const Config& cfg);
 void apply_config_entry(Config* cfg, const std::string& key, const std::string& value);
 void load_config_file(Config* cfg, const std::string& path);
 
+// Page-locked host memory for frame pixels, from a size-keyed pool, so a
+// frame can be DMA'd to the GPU straight from its flk_image (no staging copy).
+// Falls back to ordinary memory when pinning is unavailable (no driver /
+// device, or the pinned budget is exhausted).
+void* pinned_acquire(size_t bytes);
+void pinned_release(void* p, size_t bytes) noexcept;
+bool pinned_contains(const void* p);
+
+template <class T>
+struct PinnedAlloc {
+  using value_type = T;
+  PinnedAlloc() = default;
+  template <class U>
+  PinnedAlloc(const PinnedAlloc<U>&) {}
+  T* allocate(size_t n) { return static_cast<T*>(pinned_acquire(n * sizeof(T))); }
+  void deallocate(T* p, size_t n) noexcept { pinned_release(p, n * sizeof(T)); }
+  template <class U>
+  bool operator==(const PinnedAlloc<U>&) const { return true; }
+  template <class U>
+  bool operator!=(const PinnedAlloc<U>&) const { return false; }
+};
+
 // Tightly packed host raster (the C ABI copies into this, capi.cpp:134-149).
 struct HostImage {
   int width = 0;
   int height = 0;
-  std::vector<uint8_t> px;
+  std::vector<uint8_t, PinnedAlloc<uint8_t>> px;
+  bool pinned() const { return !px.empty() && pinned_contains(px.data()); }
 };
 
 HostImage make_image(int width, int height, const uint8_t* pixels);

@@ -7,9 +7,16 @@
 // range checks at detector creation (fast.cpp:18-27, nms.cpp:13-23,
 // lk.cpp:36-46, frontend.cpp:26-36) and the binary-PGM reader
 // (image.cpp:86-170).
+#include <cuda_runtime.h>
+
 #include <cctype>
 #include <cstdio>
+#include <cstdlib>
 #include <fstream>
+#include <map>
+#include <mutex>
+#include <new>
+#include <unordered_set>
 
 #include "common.hpp"
 
@@ -127,6 +134,82 @@ void load_config_file(Config* c, const std::string& path) {
       throw ConfigError(where + e.what());
     }
   }
+}
+
+// ------------------------------------------------------------ pinned pool
+
+namespace {
+
+struct PinnedPool {
+  std::mutex mu;
+  std::multimap<size_t, void*> free_blocks;  // size -> cached pinned block
+  std::unordered_set<const void*> pinned;    // every live or cached pinned block
+  size_t cached = 0;
+  int state = 0;  // 0 untried, 1 pinning works, -1 unavailable
+  static constexpr size_t kMaxCached = size_t(256) << 20;
+  static constexpr size_t kMaxPinned = size_t(8) << 30;
+  size_t live_pinned = 0;
+};
+
+PinnedPool& pool() {
+  static PinnedPool* p = new PinnedPool();  // never destroyed: blocks outlive static teardown
+  return *p;
+}
+
+}  // namespace
+
+void* pinned_acquire(size_t bytes) {
+  if (bytes == 0) bytes = 1;
+  PinnedPool& P = pool();
+  {
+    std::lock_guard<std::mutex> lk(P.mu);
+    auto it = P.free_blocks.find(bytes);
+    if (it != P.free_blocks.end()) {
+      void* p = it->second;
+      P.free_blocks.erase(it);
+      P.cached -= bytes;
+      return p;
+    }
+    if (P.state >= 0 && P.live_pinned + bytes <= PinnedPool::kMaxPinned) {
+      void* p = nullptr;
+      if (cudaHostAlloc(&p, bytes, cudaHostAllocPortable) == cudaSuccess) {
+        P.state = 1;
+        P.pinned.insert(p);
+        P.live_pinned += bytes;
+        return p;
+      }
+      cudaGetLastError();  // clear the failed call
+      if (P.state == 0) P.state = -1;  // no usable driver / device: stop trying
+    }
+  }
+  void* p = std::malloc(bytes);
+  if (!p) throw std::bad_alloc();
+  return p;
+}
+
+void pinned_release(void* p, size_t bytes) noexcept {
+  if (!p) return;
+  if (bytes == 0) bytes = 1;
+  PinnedPool& P = pool();
+  std::lock_guard<std::mutex> lk(P.mu);
+  if (P.pinned.count(p) == 0) {
+    std::free(p);
+    return;
+  }
+  if (P.cached + bytes <= PinnedPool::kMaxCached) {
+    P.free_blocks.emplace(bytes, p);
+    P.cached += bytes;
+    return;
+  }
+  P.pinned.erase(p);
+  P.live_pinned -= bytes;
+  cudaFreeHost(p);
+}
+
+bool pinned_contains(const void* p) {
+  PinnedPool& P = pool();
+  std::lock_guard<std::mutex> lk(P.mu);
+  return P.pinned.count(p) != 0;
 }
 
 HostImage make_image(int width, int height, const uint8_t* pixels) {

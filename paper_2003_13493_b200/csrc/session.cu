@@ -412,9 +412,8 @@ void Session::capture_frame_graph() {
     cudaGraph_t graph = nullptr;
     check_cuda(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal), "capture");
     try {
-      mark(0);
-      check_cuda(cudaMemcpyAsync(d_frame_, h_frame_, frame_bytes, cudaMemcpyHostToDevice, stream_),
-                 "H2D frame");
+      // (the frame's H2D and the first stage event are enqueued before each
+      // replay: the copy's source is the image itself when it is page-locked)
       graph_launches_ = batch_->enqueue_pyramid(d_frame_, frame_bytes, pitch_, 1, stream_, 0);
       mark(1);
       check_cuda(cudaMemcpyAsync(d_io_, h_io_, io_bytes, cudaMemcpyHostToDevice, stream_),
@@ -478,11 +477,20 @@ void Session::submit(const HostImage& img, bool timed) {
   // Stage times are CUDA-event device times.
   static const bool trace = std::getenv("FLKB_SESSION_TRACE") != nullptr;
   const auto tt0 = Clock::now();
-  // rows re-pitched on the host, then one contiguous DMA (a pitched 2-D copy
-  // of a small frame costs the copy engine several times longer)
-  for (int y = 0; y < img.height; ++y)
-    std::memcpy(h_frame_ + static_cast<size_t>(y) * pitch_,
-                img.px.data() + static_cast<size_t>(y) * img.width, img.width);
+  // one contiguous DMA of the frame at the device pitch, straight from the
+  // image's page-locked pixels when the rows already have that pitch, else
+  // re-pitched through the pinned staging buffer (a pitched 2-D copy of a
+  // small frame costs the copy engine several times longer)
+  const uint8_t* src = img.px.data();
+  if (!(pitch_ == img.width && img.pinned())) {
+    for (int y = 0; y < img.height; ++y)
+      std::memcpy(h_frame_ + static_cast<size_t>(y) * pitch_,
+                  img.px.data() + static_cast<size_t>(y) * img.width, img.width);
+    src = h_frame_;
+  }
+  if (timed) check_cuda(cudaEventRecord(ev_[0], stream_), "event");
+  check_cuda(cudaMemcpyAsync(d_frame_, src, static_cast<size_t>(pitch_) * img.height,
+                             cudaMemcpyHostToDevice, stream_), "H2D frame");
   const auto tt1 = Clock::now();
   const int n = static_cast<int>(tracks_.size());
   *reinterpret_cast<int*>(h_io_) = n;
