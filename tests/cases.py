@@ -67,4 +67,7 @@ SESSIONS = [
                                                    ratio=0.9)),
     ("noise_l3_n2", "noise", 6, 256, 192, _scfg(l=3, h=8, target=40, n=2)),
     ("c2_752x480_l3", "slide2", 8, 752, 480, _scfg(l=3, h=8, target=200, ratio=0.6)),
+    ("c2_752x480_l3_long", "slide2", 40, 752, 480, _scfg(l=3, h=8, target=200, ratio=0.3)),
+    ("drift_l4_w2_h4_sada", "drift", 12, 640, 480, _scfg(l=4, w=2, h=4, target=50, ratio=0.7,
+                                                         score_kind="sad_a", N=11)),
 ]

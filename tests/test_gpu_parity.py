@@ -56,7 +56,7 @@ def test_golden_cases_through_c_abi(golden, case, fuse, monkeypatch):
     assert (again == feats).all()
 
 
-@pytest.mark.parametrize("seed", range(16))
+@pytest.mark.parametrize("seed", range(48))
 def test_random_configs_vs_oracle(orc, seed, monkeypatch):
     monkeypatch.setenv("FLKB_FUSE_PYR", str(seed % 2))
     rng = np.random.default_rng(500 + seed)
