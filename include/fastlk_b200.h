@@ -32,8 +32,9 @@ FLK_API int flkb_device_count(void);
 
 /* Many host frames in one call: images must all have the detector's frame
  * size. outs[i] receives frame i's features (caller frees each); stats may be
- * NULL or an array of n. Frames are pipelined through pinned staging buffers
- * so H2D, compute and D2H overlap. */
+ * NULL or an array of n. Frames go through a two-slot pipeline kept by the
+ * detector (H2D of one chunk overlaps the kernels of the other); images whose
+ * page-locked pixels already have the device pitch are DMA'd in place. */
 FLK_API flk_status flkb_detector_run_batch(flk_detector* detector,
                                            const flk_image* const* images, int n,
                                            flk_features** outs, flk_frame_stats* stats);
@@ -112,6 +113,12 @@ FLK_API flk_status flkb_detector_responses(flk_detector* detector, const flk_ima
 FLK_API flk_status flkb_sessions_process(flk_session* const* sessions,
                                          const flk_image* const* images, int n,
                                          flk_tracks** out_tracks, flk_frame_stats* stats);
+
+/* Bulk accessors: copy min(count, cap) records into out (row-major cell
+ * order / id order, as flk_features_get / flk_tracks_get index them) and
+ * return the number copied; NULL handles copy nothing. */
+FLK_API int flkb_features_copy(const flk_features* features, flk_feature* out, int cap);
+FLK_API int flkb_tracks_copy(const flk_tracks* tracks, flk_track_info* out, int cap);
 
 /* Number of CUDA kernels this library has launched in the process (graph
  * replays count every kernel node). */

@@ -9,6 +9,7 @@
 // flk_detector_run are those of capi.cpp:232-274.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstring>
 #include <memory>
 #include <new>
@@ -185,6 +186,8 @@ class FrameRunner {
   cudaGraphExec_t exec_ = nullptr;
 };
 
+class BatchPipeline;
+
 int current_device() {
   int n = 0;
   cudaError_t e = cudaGetDeviceCount(&n);
@@ -216,6 +219,7 @@ struct flk_detector {
   int first_width = 0;
   int first_height = 0;
   std::unique_ptr<FrameRunner> runner;
+  std::unique_ptr<BatchPipeline> pipeline;  // flkb_detector_run_batch
 };
 struct flk_session {
   std::unique_ptr<flkb::Session> session;
@@ -244,6 +248,105 @@ struct flkb_batch {
     if (cur >= 0) cudaSetDevice(cur);
   }
 };
+
+namespace {
+
+// The host-batch pipeline of one detector (flkb_detector_run_batch), kept
+// across calls: two slots of up to kChunk frames, each with its device
+// workspace, input buffer, pinned staging / result buffers and stream, so
+// slot A's kernels run while slot B's frames are copied in. Frames whose
+// page-locked pixels already have the device pitch are DMA'd straight from
+// the image; others are staged.
+class BatchPipeline {
+ public:
+  static constexpr int kChunk = 128;
+  BatchPipeline(const flkb::DetectParams& p, int device, int w, int h)
+      : device_(device), w_(w), h_(h) {
+    flkb::DeviceGuard guard(device_);
+    pitch_ = static_cast<int>(round16(static_cast<size_t>(w)));
+    fs_ = static_cast<size_t>(pitch_) * h;
+    cells_ = flkb::Geometry::make(p, w, h).cells;
+    for (auto& sl : slots_) {
+      sl.b = std::make_unique<flkb::DeviceBatch>(p, device, w, h, kChunk);
+      flkb::check_cuda(cudaStreamCreateWithFlags(&sl.s, cudaStreamNonBlocking), "stream");
+      flkb::check_cuda(cudaMalloc(&sl.d_in, fs_ * kChunk + 16), "batch input");
+      sl.in.ensure(fs_ * kChunk);
+      sl.out.ensure(sizeof(int) * kChunk + sizeof(flk_feature) * static_cast<size_t>(cells_) * kChunk);
+    }
+  }
+  ~BatchPipeline() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    cudaSetDevice(device_);
+    for (auto& sl : slots_) {
+      if (sl.s) cudaStreamDestroy(sl.s);
+      cudaFree(sl.d_in);
+      sl.b.reset();
+    }
+    if (cur >= 0) cudaSetDevice(cur);
+  }
+
+  void run(const flk_image* const* images, int n, flk_features** outs) {
+    flkb::DeviceGuard guard(device_);
+    for (auto& sl : slots_) sl.first = -1;
+    int si = 0;
+    for (int c0 = 0; c0 < n; c0 += kChunk, si ^= 1) {
+      Slot& sl = slots_[si];
+      drain(sl, outs);
+      const int cnt = std::min(kChunk, n - c0);
+      uint8_t* hp = static_cast<uint8_t*>(sl.in.p);
+      for (int j = 0; j < cnt; ++j) {
+        const flkb::HostImage& img = images[c0 + j]->img;
+        const uint8_t* src = img.px.data();
+        if (!(pitch_ == w_ && img.pinned())) {
+          uint8_t* dst = hp + static_cast<size_t>(j) * fs_;
+          for (int y = 0; y < h_; ++y)
+            std::memcpy(dst + static_cast<size_t>(y) * pitch_, src + static_cast<size_t>(y) * w_, w_);
+          src = dst;
+        }
+        flkb::check_cuda(cudaMemcpyAsync(sl.d_in + static_cast<size_t>(j) * fs_, src, fs_,
+                                         cudaMemcpyHostToDevice, sl.s), "H2D batch frame");
+      }
+      sl.b->run(sl.d_in, fs_, pitch_, cnt, false, sl.s);
+      sl.b->download(0, cnt, static_cast<int*>(sl.out.p), results(sl), sl.s);
+      sl.first = c0;
+      sl.count = cnt;
+    }
+    drain(slots_[si], outs);
+    drain(slots_[si ^ 1], outs);
+  }
+
+ private:
+  struct Slot {
+    std::unique_ptr<flkb::DeviceBatch> b;
+    uint8_t* d_in = nullptr;
+    Pinned in, out;
+    cudaStream_t s = nullptr;
+    int first = -1, count = 0;
+  };
+  flk_feature* results(Slot& sl) {
+    return reinterpret_cast<flk_feature*>(static_cast<char*>(sl.out.p) + sizeof(int) * kChunk);
+  }
+  void drain(Slot& sl, flk_features** outs) {
+    if (sl.first < 0) return;
+    flkb::check_cuda(cudaStreamSynchronize(sl.s), "batch sync");
+    const int* counts = static_cast<const int*>(sl.out.p);
+    const flk_feature* fv = results(sl);
+    for (int j = 0; j < sl.count; ++j) {
+      auto f = std::make_unique<flk_features>();
+      const flk_feature* b = fv + static_cast<size_t>(j) * cells_;
+      f->items.assign(b, b + counts[j]);
+      outs[sl.first + j] = f.release();
+    }
+    sl.first = -1;
+  }
+
+  int device_, w_, h_, pitch_ = 0, cells_ = 0;
+  size_t fs_ = 0;
+  Slot slots_[2];
+};
+
+}  // namespace
 
 extern "C" {
 
@@ -382,6 +485,20 @@ flk_status flk_features_get(const flk_features* features, int index, flk_feature
 }
 
 void flk_features_destroy(flk_features* features) { delete features; }
+
+int flkb_features_copy(const flk_features* features, flk_feature* out, int cap) {
+  if (!features || !out || cap <= 0) return 0;
+  const int n = std::min(cap, static_cast<int>(features->items.size()));
+  std::memcpy(out, features->items.data(), sizeof(flk_feature) * static_cast<size_t>(n));
+  return n;
+}
+
+int flkb_tracks_copy(const flk_tracks* tracks, flk_track_info* out, int cap) {
+  if (!tracks || !out || cap <= 0) return 0;
+  const int n = std::min(cap, static_cast<int>(tracks->items.size()));
+  std::memcpy(out, tracks->items.data(), sizeof(flk_track_info) * static_cast<size_t>(n));
+  return n;
+}
 
 /* --------------------------------------------------------------- tracking */
 
@@ -538,78 +655,19 @@ flk_status flkb_detector_run_batch(flk_detector* detector, const flk_image* cons
       }
       return FLK_OK;
     }
-    flkb::DeviceGuard guard(detector->device);
-    // Two pipeline slots of up to kChunk frames: while slot A's kernels run,
-    // slot B's frames are staged and copied.
-    constexpr int kChunk = 64;
-    const int chunk = std::min(kChunk, n);
-    const int pitch = static_cast<int>(round16(static_cast<size_t>(W)));
-    const size_t fs = static_cast<size_t>(pitch) * H;
-    struct Slot {
-      std::unique_ptr<flkb::DeviceBatch> b;
-      uint8_t* d_in = nullptr;
-      Pinned in, out;
-      cudaStream_t s = nullptr;
-      int first = -1, count = 0;
-    } slots[2];
-    auto cleanup = [&] {
-      for (auto& sl : slots) {
-        if (sl.s) cudaStreamDestroy(sl.s);
-        cudaFree(sl.d_in);
-      }
-    };
+    if (!detector->pipeline)
+      detector->pipeline = std::make_unique<BatchPipeline>(detector->params, detector->device,
+                                                           detector->first_width,
+                                                           detector->first_height);
     try {
-      const int cells = flkb::Geometry::make(detector->params, W, H).cells;
-      for (auto& sl : slots) {
-        sl.b = std::make_unique<flkb::DeviceBatch>(detector->params, detector->device, W, H, chunk);
-        flkb::check_cuda(cudaStreamCreateWithFlags(&sl.s, cudaStreamNonBlocking), "stream");
-        flkb::check_cuda(cudaMalloc(&sl.d_in, fs * chunk + 16), "batch input");
-        sl.in.ensure(static_cast<size_t>(W) * H * chunk);
-        sl.out.ensure(sizeof(int) * chunk + sizeof(flk_feature) * static_cast<size_t>(cells) * chunk);
-      }
-      auto drain = [&](Slot& sl) {
-        if (sl.first < 0) return;
-        flkb::check_cuda(cudaStreamSynchronize(sl.s), "batch sync");
-        const int* counts = static_cast<const int*>(sl.out.p);
-        const flk_feature* fv = reinterpret_cast<const flk_feature*>(
-            static_cast<const char*>(sl.out.p) + sizeof(int) * chunk);
-        for (int j = 0; j < sl.count; ++j) {
-          auto f = std::make_unique<flk_features>();
-          const flk_feature* b = fv + static_cast<size_t>(j) * cells;
-          f->items.assign(b, b + counts[j]);
-          outs[sl.first + j] = f.release();
-        }
-        sl.first = -1;
-      };
-      int si = 0;
-      for (int c0 = 0; c0 < n; c0 += chunk, si ^= 1) {
-        Slot& sl = slots[si];
-        drain(sl);
-        const int cnt = std::min(chunk, n - c0);
-        uint8_t* hp = static_cast<uint8_t*>(sl.in.p);
-        for (int j = 0; j < cnt; ++j)
-          std::memcpy(hp + static_cast<size_t>(j) * W * H, images[c0 + j]->img.px.data(),
-                      static_cast<size_t>(W) * H);
-        flkb::check_cuda(cudaMemcpy2DAsync(sl.d_in, pitch, hp, W, W, static_cast<size_t>(H) * cnt,
-                                           cudaMemcpyHostToDevice, sl.s), "H2D batch");
-        sl.b->run(sl.d_in, fs, pitch, cnt, false, sl.s);
-        sl.b->download(0, cnt, static_cast<int*>(sl.out.p),
-                       reinterpret_cast<flk_feature*>(static_cast<char*>(sl.out.p) + sizeof(int) * chunk),
-                       sl.s);
-        sl.first = c0;
-        sl.count = cnt;
-      }
-      drain(slots[si]);
-      drain(slots[si ^ 1]);
+      detector->pipeline->run(images, n, outs);
     } catch (...) {
       for (int i = 0; i < n; ++i) {
         flk_features_destroy(outs[i]);
         outs[i] = nullptr;
       }
-      cleanup();
       throw;
     }
-    cleanup();
     return FLK_OK;
   });
 }

@@ -103,7 +103,7 @@ EXT_SYMBOLS = [
     "flkb_batch_device_counts", "flkb_batch_device_features", "flkb_batch_device_stats",
     "flkb_batch_device_pyramid", "flkb_synth_frames_device", "flkb_kernel_launch_count",
     "flkb_batch_kernels_per_run", "flkb_detector_responses", "flkb_batch_run_device_timed",
-    "flkb_sessions_process"]
+    "flkb_sessions_process", "flkb_features_copy", "flkb_tracks_copy"]
 
 _lib = None
 _vp = ctypes.c_void_p
@@ -176,6 +176,8 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.flk_tracks_get.argtypes = [_vp, ctypes.c_int, _vp]
     lib.flk_track_status_name.argtypes = [ctypes.c_int]
     lib.flkb_sessions_process.argtypes = [_vp, _vp, ctypes.c_int, _vp, _vp]
+    lib.flkb_features_copy.argtypes = [_vp, _vp, ctypes.c_int]
+    lib.flkb_tracks_copy.argtypes = [_vp, _vp, ctypes.c_int]
     lib.flkb_synth_frames_device.argtypes = [_vp, ctypes.c_int, ctypes.c_uint64, ctypes.c_int,
                                              ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                              ctypes.c_size_t, _vp]
@@ -285,10 +287,16 @@ class Image(_Handle):
 def _features_to_array(handle) -> np.ndarray:
     n = _lib.flk_features_count(handle)
     out = np.zeros(n, FEATURE_DTYPE)
-    f = Feature()
-    for i in range(n):
-        _check(_lib.flk_features_get(handle, i, ctypes.byref(f)))
-        out[i] = (f.x, f.y, f.score, f.level, f.cell_x, f.cell_y)
+    if n:
+        assert _lib.flkb_features_copy(handle, out.ctypes.data, n) == n
+    return out
+
+
+def _tracks_to_array(handle) -> np.ndarray:
+    n = _lib.flk_tracks_count(handle)
+    out = np.zeros(n, TRACK_DTYPE)
+    if n:
+        assert _lib.flkb_tracks_copy(handle, out.ctypes.data, n) == n
     return out
 
 
@@ -320,10 +328,7 @@ class Session(_Handle):
                                         ctypes.byref(st) if st is not None else None,
                                         ctypes.byref(cf) if cf is not None else None))
         try:
-            n = _lib.flk_tracks_count(th)
-            out = np.zeros(n, TRACK_DTYPE)
-            for i in range(n):
-                _check(_lib.flk_tracks_get(th, i, out[i:].ctypes.data))
+            out = _tracks_to_array(th)
         finally:
             _lib.flk_tracks_destroy(th)
         extra = {}
@@ -347,13 +352,9 @@ def sessions_process(sessions, images):
     for i in range(n):
         th = _vp(outs[i])
         try:
-            m = _lib.flk_tracks_count(th)
-            out = np.zeros(m, TRACK_DTYPE)
-            for j in range(m):
-                _check(_lib.flk_tracks_get(th, j, out[j:].ctypes.data))
+            res.append(_tracks_to_array(th))
         finally:
             _lib.flk_tracks_destroy(th)
-        res.append(out)
     return res
 
 
