@@ -213,6 +213,8 @@ fused::Params fused_geometry(const DetectParams& p, const Geometry& g, int R, in
   P.sw = static_cast<int>(round_up(
       static_cast<size_t>(std::max(fused::kOwn * (P.nw_max - 1) + 36, tw_max + 2 * n + 22)), 16));
   P.rp = static_cast<int>(round_up(static_cast<size_t>(tw_max + 4 * n), 8));
+  // the radius-1 instance has compile-time pitches; layouts that fit are padded to them
+  if (n == 1 && P.sw <= fused::kSw1 && P.rp <= fused::kRp1) P.sw = fused::kSw1, P.rp = fused::kRp1;
   // 32-bit in-cell keys need cells of at most 1024 px per side
   // 32-bit in-CTA keys (score << 20 | 10-bit y and x offsets inside the CTA)
   P.key_slots = slots <= 4096 ? slots : 0;
@@ -327,11 +329,14 @@ void DeviceBatch::run(const uint8_t* frames, size_t fstride, int pitch, int coun
     run_staged(frames, fstride, pitch, count, stats, s, times, first);
     return;
   }
-  const fused::KernelFn kern = fused::kernel_for(p_.arc_length, p_.score, p_.radius);
-  if (static_cast<size_t>(smem) > fused_smem_) {
+  const bool fixed_pitch = p_.radius == 1 && P.sw == fused::kSw1 && P.rp == fused::kRp1;
+  const fused::KernelFn kern = fused::kernel_for(p_.arc_length, p_.score, fixed_pitch ? 1 : 0);
+  if (reinterpret_cast<const void*>(kern) != fused_kern_ || static_cast<size_t>(smem) > fused_smem_) {
     check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
                "fused smem attribute");
-    fused_smem_ = static_cast<size_t>(smem);
+    if (reinterpret_cast<const void*>(kern) != fused_kern_) fused_smem_ = 0;
+    fused_kern_ = reinterpret_cast<const void*>(kern);
+    fused_smem_ = std::max(fused_smem_, static_cast<size_t>(smem));
   }
   uint8_t* pyr = d_pyr_ ? d_pyr_ + static_cast<size_t>(first) * g_.pyr_frame_bytes : nullptr;
   unsigned long long* keys = d_keys_ + static_cast<size_t>(first) * g_.cells;

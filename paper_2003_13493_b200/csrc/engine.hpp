@@ -125,6 +125,7 @@ class DeviceBatch {
   int* d_counts_ = nullptr;
   uint64_t* d_stats_ = nullptr;  // [capacity][2] = candidates, comparisons
   float* d_naive_ = nullptr;     // conformance scratch (lazily allocated)
+  const void* fused_kern_ = nullptr;  // kernel the smem attribute below was set on
   size_t fused_smem_ = 0;        // dynamic shared memory of the fused kernel
   int fused_R_ = 32;             // rows per band (cheapest shape that fits kMinBlocks CTAs/SM)
   int fused_tiles0_ = 0;         // level-0 column tiles of that shape (0 = not chosen yet)

@@ -48,6 +48,10 @@ constexpr int kWarps = kThreads / 32;
 #endif
 constexpr int kMinBlocks = FLKB_MIN_BLOCKS;  // CTAs per SM the register budget targets
 constexpr int kMaxLv = 16;
+// Stage pitch (bytes) and score-tile pitch (u16) of the radius-1 instance:
+// column tiles up to 192 px (8 plane words) fit them.
+constexpr int kSw1 = 224;
+constexpr int kRp1 = 200;
 
 // Exact x / d for 0 <= x < 2^31 with one IMAD.HI: q = (umulhi(x, m) + x) >> l,
 // l = ceil(log2 d), m = 1 + floor(2^32 (2^l - d) / d).
@@ -314,6 +318,11 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_detect(const __grid_co
   const Smem S = smem_layout(P);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 
+  // stage / score-tile pitches: compile-time in the radius-1 instance (the host
+  // pads the layout to them), so ring and window loads take immediate offsets
+  const int SW = RADIUS == 1 ? kSw1 : P.sw;
+  const int RP = RADIUS == 1 ? kRp1 : P.rp;
+
   // --- which level, band and column tile
   int k = P.k_begin;
   while (k + 1 < P.k_end && static_cast<int>(blockIdx.x) >= P.lv[k + 1].cta0) ++k;
@@ -354,7 +363,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_detect(const __grid_co
   const uint8_t* frame = L.img + f * L.fstride;
   const int gx0 = max(bx0, 0);
   const int sx0 = gx0 - bx0;  // multiple of 16
-  int row_bytes = min(bx0 + P.sw, L.pitch) - gx0;
+  int row_bytes = min(bx0 + SW, L.pitch) - gx0;
   row_bytes = min(row_bytes, ((w + 15) & ~15) - gx0);
   if (L.tma) {
     row_bytes &= ~15;
@@ -370,7 +379,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_detect(const __grid_co
   } else {
     for (int i = tid; i < (yb - ya) * row_bytes; i += kThreads) {
       const int y = ya + i / row_bytes, x = i % row_bytes;
-      stage[(y - iy0) * P.sw + sx0 + x] = frame[static_cast<size_t>(y) * L.pitch + gx0 + x];
+      stage[(y - iy0) * SW + sx0 + x] = frame[static_cast<size_t>(y) * L.pitch + gx0 + x];
     }
   }
   if (local_keys)
@@ -382,7 +391,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_detect(const __grid_co
     const uint32_t b = static_cast<uint32_t>(__cvta_generic_to_shared(bar));
     for (int y = ya + tid; y < yb; y += kThreads) {
       const uint32_t dst = static_cast<uint32_t>(
-          __cvta_generic_to_shared(stage + (y - iy0) * P.sw + sx0));
+          __cvta_generic_to_shared(stage + (y - iy0) * SW + sx0));
       const uint8_t* src = frame + static_cast<size_t>(y) * L.pitch + gx0;
       asm volatile(
           "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
@@ -415,11 +424,11 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_detect(const __grid_co
       // more than the float error for i < 2^16
       const int by = __float2int_rz((static_cast<float>(i) + 0.5f) * inv_bxn), bxi = i - by * bxn;
       const int x = x_lo + 16 * bxi, y = y0 + 4 * by;
-      const uint8_t* sp = stage + (y - iy0) * P.sw + (x - bx0);
+      const uint8_t* sp = stage + (y - iy0) * SW + (x - bx0);
       const uint4 r0 = *reinterpret_cast<const uint4*>(sp);
-      const uint4 r1 = *reinterpret_cast<const uint4*>(sp + P.sw);
-      const uint4 r2 = *reinterpret_cast<const uint4*>(sp + 2 * P.sw);
-      const uint4 r3 = *reinterpret_cast<const uint4*>(sp + 3 * P.sw);
+      const uint4 r1 = *reinterpret_cast<const uint4*>(sp + SW);
+      const uint4 r2 = *reinterpret_cast<const uint4*>(sp + 2 * SW);
+      const uint4 r3 = *reinterpret_cast<const uint4*>(sp + 3 * SW);
       const uint32_t a0 = down4(r0.x, r0.y, r1.x, r1.y), a1 = down4(r0.z, r0.w, r1.z, r1.w);
       const uint32_t b0 = down4(r2.x, r2.y, r3.x, r3.y), b1 = down4(r2.z, r2.w, r3.z, r3.w);
       const int X1 = x >> 1, Y1 = y >> 1;
@@ -455,7 +464,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_detect(const __grid_co
     for (int t = tid; t < tasks; t += kThreads, it.next()) {
       const int r = ya - iy0 + it.row, j = it.j;
       const int bx = kOwn * j;
-      const uint32_t* src = reinterpret_cast<const uint32_t*>(stage + r * P.sw + (bx & ~3));
+      const uint32_t* src = reinterpret_cast<const uint32_t*>(stage + r * SW + (bx & ~3));
       uint32_t a[9], wv[8], pl[8];
 #pragma unroll
       for (int i = 0; i < 9; ++i) a[i] = src[i];
@@ -555,7 +564,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_detect(const __grid_co
   }
   {
     uint4* z = reinterpret_cast<uint4*>(tile_s);
-    const int n16 = ((P.R + 2 * n) * P.rp * 2) / 16;
+    const int n16 = ((P.R + 2 * n) * RP * 2) / 16;
     for (int i = tid; i < n16; i += kThreads) z[i] = make_uint4(0, 0, 0, 0);
   }
   int incl = cnt;
@@ -669,13 +678,13 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_detect(const __grid_co
     for (int e = tid; e < m_end; e += kThreads) {
       const int ent = list[e];
       const int y = cy_lo + (ent >> 10), xs = ent & 1023;
-      const uint8_t* sp = stage + (y - iy0) * P.sw + xs;
+      const uint8_t* sp = stage + (y - iy0) * SW + xs;
       const uint32_t cc = sp[0];
       int sc;
       if (KIND == kSadB) {
         uint32_t rb[16];
 #pragma unroll
-        for (int i = 0; i < 16; ++i) rb[i] = sp[ring_dy(i) * P.sw + ring_dx(i)];
+        for (int i = 0; i < 16; ++i) rb[i] = sp[ring_dy(i) * SW + ring_dx(i)];
         uint32_t pk[4];
 #pragma unroll
         for (int q = 0; q < 4; ++q)  // bytes packed with IMAD (FMA pipe; the ALU pipe is the busy one)
@@ -685,10 +694,10 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_detect(const __grid_co
       } else {
         int ring[16];
 #pragma unroll
-        for (int i = 0; i < 16; ++i) ring[i] = sp[ring_dy(i) * P.sw + ring_dx(i)];
+        for (int i = 0; i < 16; ++i) ring[i] = sp[ring_dy(i) * SW + ring_dx(i)];
         sc = fast_score<N, KIND>(static_cast<int>(cc), ring, P.eps);
       }
-      tile_s[(y - fy0) * P.rp + xs + tcol] = static_cast<uint16_t>(sc);
+      tile_s[(y - fy0) * RP + xs + tcol] = static_cast<uint16_t>(sc);
     }
   }
   __syncthreads();
@@ -700,7 +709,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_detect(const __grid_co
     const int nx_lo = max(x_lo, 3), nx_hi = min(x_hi, w - 3);
     const int e_lo = T1 > T0 ? scan[kWarps + 1] : 0;
     const int e_hi = T1 > T0 ? scan[kWarps + 2] : 0;
-    const int rp = P.rp;
+    const int rp = RP;
     const uint32_t kc = static_cast<uint32_t>((1023 + y0) * 1024 + 1023 + x_lo);
     const uint32_t pk = P.pow2[k];  // level -> level-0 coordinates
     for (int w0 = e_lo; w0 < e_hi; w0 += cap) {
