@@ -62,7 +62,7 @@ struct Pinned {
     if (p) cudaFreeHost(p);
     p = nullptr;
     bytes = 0;
-    flkb::check_cuda(cudaMallocHost(&p, n), "cudaMallocHost");
+    flkb::check_cuda(cudaHostAlloc(&p, n, cudaHostAllocMapped), "cudaHostAlloc");
     bytes = n;
   }
   ~Pinned() {
@@ -105,19 +105,22 @@ class FrameRunner {
     flk_feature* fv = reinterpret_cast<flk_feature*>(static_cast<char*>(out_.p) + 4 * sizeof(int));
     const int cells = batch_.geometry().cells;
     uint64_t* st = reinterpret_cast<uint64_t*>(fv + cells);
-    if (stats == nullptr) {
+    if (stats == nullptr && conf == nullptr) {
       if (!exec_) capture();
       flkb::check_cuda(cudaGraphLaunch(exec_, stream_), "cudaGraphLaunch");
       flkb::count_launches(batch_.kernels_per_run());
-    } else {
+    } else {  // the conformance pass reads the device feature list
       flkb::StageTimes t;
-      batch_.run(d_in_, static_cast<size_t>(pitch_) * h_, pitch_, 1, true, stream_, &t);
+      batch_.run(d_in_, static_cast<size_t>(pitch_) * h_, pitch_, 1, stats != nullptr, stream_,
+                 stats ? &t : nullptr);
       batch_.download(0, 1, counts, fv, stream_);
-      flkb::check_cuda(cudaMemcpyAsync(st, batch_.device_stats(), 2 * sizeof(uint64_t),
-                                       cudaMemcpyDeviceToHost, stream_), "download stats");
-      stats->pyramid_us = t.pyramid_us;
-      stats->crf_us = t.crf_us;
-      stats->nms_us = t.nms_us;
+      if (stats) {
+        flkb::check_cuda(cudaMemcpyAsync(st, batch_.device_stats(), 2 * sizeof(uint64_t),
+                                         cudaMemcpyDeviceToHost, stream_), "download stats");
+        stats->pyramid_us = t.pyramid_us;
+        stats->crf_us = t.crf_us;
+        stats->nms_us = t.nms_us;
+      }
     }
     flkb::check_cuda(cudaStreamSynchronize(stream_), "cudaStreamSynchronize");
     const int n = counts[0];
@@ -162,9 +165,18 @@ class FrameRunner {
     int* counts = static_cast<int*>(out_.p);
     flk_feature* fv = reinterpret_cast<flk_feature*>(static_cast<char*>(out_.p) + 4 * sizeof(int));
     flkb::check_cuda(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal), "capture");
-    try {  // the frame's H2D precedes each replay (its source may change)
-      batch_.run(d_in_, static_cast<size_t>(pitch_) * h_, pitch_, 1, false, stream_);
-      batch_.download(0, 1, counts, fv, stream_);
+    try {
+      // The frame's H2D precedes each replay (its source may change). The
+      // compaction writes the count and the feature list straight into the
+      // mapped page-locked output: no device-to-host copies to schedule.
+      int* dc = nullptr;
+      flk_feature* df = nullptr;
+      flkb::check_cuda(cudaHostGetDevicePointer(reinterpret_cast<void**>(&dc), counts, 0),
+                       "mapped counts");
+      flkb::check_cuda(cudaHostGetDevicePointer(reinterpret_cast<void**>(&df), fv, 0),
+                       "mapped features");
+      batch_.run(d_in_, static_cast<size_t>(pitch_) * h_, pitch_, 1, false, stream_, nullptr, 0,
+                 false, dc, df);
     } catch (...) {
       cudaGraph_t g = nullptr;
       cudaStreamEndCapture(stream_, &g);

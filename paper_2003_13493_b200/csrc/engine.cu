@@ -264,7 +264,8 @@ void DeviceBatch::build_pyramid(const uint8_t* frames, size_t fstride, int pitch
 }
 
 void DeviceBatch::run(const uint8_t* frames, size_t fstride, int pitch, int count, bool stats,
-                      cudaStream_t s, StageTimes* times, int first, bool pyramid_ready) {
+                      cudaStream_t s, StageTimes* times, int first, bool pyramid_ready,
+                      int* out_counts, flk_feature* out_feats) {
   if (count < 1 || first < 0 || first + count > capacity_)
     throw InvalidArgument("batch count " + std::to_string(count) + " outside [1, " +
                           std::to_string(capacity_) + "]");
@@ -327,6 +328,13 @@ void DeviceBatch::run(const uint8_t* frames, size_t fstride, int pitch, int coun
     std::fprintf(stderr, "flkb: R=%d tiles0=%d smem=%d ctas=%d\n", R, tiles0, smem, ctas_of(P));
   if (smem > kFusedSmemMax || R + 2 * p_.radius > 64) {  // pathological radius: staged kernels
     run_staged(frames, fstride, pitch, count, stats, s, times, first);
+    if (out_counts)
+      check_cuda(cudaMemcpyAsync(out_counts, d_counts_ + first, sizeof(int) * count,
+                                 cudaMemcpyDefault, s), "counts out");
+    if (out_feats)
+      check_cuda(cudaMemcpyAsync(out_feats, d_feats_ + static_cast<size_t>(first) * g_.cells,
+                                 sizeof(flk_feature) * g_.cells * count, cudaMemcpyDefault, s),
+                 "features out");
     return;
   }
   const bool fixed_pitch = p_.radius == 1 && P.sw == fused::kSw1 && P.rp == fused::kRp1;
@@ -340,8 +348,8 @@ void DeviceBatch::run(const uint8_t* frames, size_t fstride, int pitch, int coun
   }
   uint8_t* pyr = d_pyr_ ? d_pyr_ + static_cast<size_t>(first) * g_.pyr_frame_bytes : nullptr;
   unsigned long long* keys = d_keys_ + static_cast<size_t>(first) * g_.cells;
-  flk_feature* feats = d_feats_ + static_cast<size_t>(first) * g_.cells;
-  int* counts = d_counts_ + first;
+  flk_feature* feats = out_feats ? out_feats : d_feats_ + static_cast<size_t>(first) * g_.cells;
+  int* counts = out_counts ? out_counts : d_counts_ + first;
   unsigned long long* st =
       reinterpret_cast<unsigned long long*>(d_stats_ + 2 * static_cast<size_t>(first));
 

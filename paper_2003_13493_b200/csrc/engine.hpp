@@ -77,9 +77,13 @@ class DeviceBatch {
   // call synchronizes and reports per-stage device time.
   // With `pyramid_ready` the pyramid levels >= 1 of these frames are already
   // in place (build_pyramid) and are not rebuilt.
+  // With `out_counts` / `out_feats` (device-visible, e.g. mapped page-locked
+  // host memory) the compaction writes the frames' counts and feature lists
+  // there instead of the batch's device buffers.
   void run(const uint8_t* frames, size_t frame_stride, int pitch, int count, bool stats,
            cudaStream_t stream, StageTimes* times = nullptr, int first = 0,
-           bool pyramid_ready = false);
+           bool pyramid_ready = false, int* out_counts = nullptr,
+           flk_feature* out_feats = nullptr);
   // Pyramid levels >= 1 only (the tracking session's per-frame pyramid).
   void build_pyramid(const uint8_t* frames, size_t frame_stride, int pitch, int count,
                      cudaStream_t stream, int first = 0);
