@@ -192,17 +192,25 @@ __global__ void __launch_bounds__(256) k_template(Levels lv, const int* __restri
 // sums them in pixel order, and every thread then applies the identical
 // update (deterministic, no broadcast needed).
 __global__ void __launch_bounds__(256) k_track(Levels lv, const int* __restrict__ n_tracks,
-                                               TrackIO* __restrict__ io,
+                                               const TrackIO* __restrict__ io,
+                                               TrackIO* __restrict__ io_out,
                                                const TplLevel* __restrict__ hdr,
                                                const float* __restrict__ vals,
                                                const double* __restrict__ coef, TrackerParams tp) {
   __shared__ double prod[4][kMaxPx];
   __shared__ double rhs[4];
   __shared__ double hinv_s[16];
+  __shared__ TrackIO rec;
+  __shared__ int live;
   const int t = blockIdx.x, tid = threadIdx.x, L = lv.n;
-  if (t >= *n_tracks) return;  // the frame graph launches one CTA per slot
-  const int slot = io[t].slot;
-  double tx0 = io[t].w[0], ty0 = io[t].w[1], gain = io[t].w[2], offset = io[t].w[3];
+  if (tid == 0) {
+    live = *n_tracks;
+    if (t < live) rec = io[t];
+  }
+  __syncthreads();
+  if (t >= live) return;  // the frame graph launches one CTA per slot
+  const int slot = rec.slot;
+  double tx0 = rec.w[0], ty0 = rec.w[1], gain = rec.w[2], offset = rec.w[3];
   int iters = 0, status = 0;
   bool aborted = false, finest_converged = false;
   int finest = -1;
@@ -284,14 +292,13 @@ __global__ void __launch_bounds__(256) k_track(Levels lv, const int* __restrict_
     if (k == finest) finest_converged = level_converged;
   }
   if (!aborted && !finest_converged) status = 4;  // MAX_ITERATIONS
-  __syncthreads();  // every thread has read io[t] before it is overwritten
   if (tid == 0) {
-    io[t].status = status;
-    io[t].iters = iters;
-    io[t].w[0] = tx0;
-    io[t].w[1] = ty0;
-    io[t].w[2] = gain;
-    io[t].w[3] = offset;
+    io_out[t].status = status;
+    io_out[t].iters = iters;
+    io_out[t].w[0] = tx0;
+    io_out[t].w[1] = ty0;
+    io_out[t].w[2] = gain;
+    io_out[t].w[3] = offset;
   }
 }
 
@@ -375,7 +382,7 @@ void Session::setup(int width, int height) {
   io_bytes_ = kIoHeader + std::max(static_cast<size_t>(slots_) * sizeof(lk::TrackIO),
                                    static_cast<size_t>(slots_) * 3 * sizeof(int) + per * sizeof(int));
   check_cuda(cudaMalloc(&d_io_, io_bytes_), "session io");
-  check_cuda(cudaMallocHost(&h_io_, io_bytes_), "session io (pinned)");
+  check_cuda(cudaHostAlloc(&h_io_, io_bytes_, cudaHostAllocMapped), "session io (pinned)");
   free_.clear();
   for (int s = slots_ - 1; s >= 0; --s) free_.push_back(s);
   tracks_.clear();
@@ -383,9 +390,10 @@ void Session::setup(int width, int height) {
 }
 
 // The per-frame GPU work as one CUDA graph (replayed with one launch):
-// H2D frame -> pyramid -> H2D track records (count in the header) -> k_track
-// over every slot (CTAs past the live count exit) -> D2H records, with the
-// stage events inside. Shapes and pointers are fixed per session.
+// pyramid -> k_track over every slot (CTAs past the live count exit), with
+// the stage events inside. The frame and the track records (count in the
+// header) are copied ahead of each replay; k_track writes its results into
+// the mapped page-locked records. Shapes and pointers are fixed per session.
 void Session::capture_frame_graph() {
   for (int timed = 0; timed < 2; ++timed) {
     if (graph_exec_[timed]) cudaGraphExecDestroy(graph_exec_[timed]);
@@ -401,7 +409,8 @@ void Session::capture_frame_graph() {
     lv.h[k] = g.lh[k];
   }
   const size_t frame_bytes = static_cast<size_t>(pitch_) * g.height;
-  const size_t io_bytes = kIoHeader + sizeof(lk::TrackIO) * static_cast<size_t>(slots_);
+  uint8_t* m_io = nullptr;
+  check_cuda(cudaHostGetDevicePointer(reinterpret_cast<void**>(&m_io), h_io_, 0), "mapped io");
   // two variants: plain, and with stage events (external event-record nodes
   // cost the replay ~20 us, so they are only in the graph used for stats)
   for (int timed = 0; timed < 2; ++timed) {
@@ -416,14 +425,13 @@ void Session::capture_frame_graph() {
       // replay: the copy's source is the image itself when it is page-locked)
       graph_launches_ = batch_->enqueue_pyramid(d_frame_, frame_bytes, pitch_, 1, stream_, 0);
       mark(1);
-      check_cuda(cudaMemcpyAsync(d_io_, h_io_, io_bytes, cudaMemcpyHostToDevice, stream_),
-                 "H2D tracks");
+      // k_track writes the results straight into the mapped page-locked
+      // mirror: no device-to-host copy to schedule after it
       lk::k_track<<<slots_, 256, 0, stream_>>>(lv, reinterpret_cast<const int*>(d_io_),
-                                               reinterpret_cast<lk::TrackIO*>(d_io_ + kIoHeader),
+                                               reinterpret_cast<const lk::TrackIO*>(d_io_ + kIoHeader),
+                                               reinterpret_cast<lk::TrackIO*>(m_io + kIoHeader),
                                                d_hdr_, d_vals_, d_coef_, tp_);
       ++graph_launches_;
-      check_cuda(cudaMemcpyAsync(h_io_, d_io_, io_bytes, cudaMemcpyDeviceToHost, stream_),
-                 "D2H tracks");
       mark(2);
     } catch (...) {
       cudaStreamEndCapture(stream_, &graph);
@@ -473,7 +481,8 @@ void Session::submit(const HostImage& img, bool timed) {
   flk_frame_stats st{};
 
   // One submission for the pyramid and the LK launch, one synchronisation:
-  // H2D frame -> pyramid -> H2D track records -> k_track -> D2H records.
+  // H2D frame, H2D track records, then the graph: pyramid -> k_track (results
+  // written to the mapped records).
   // Stage times are CUDA-event device times.
   static const bool trace = std::getenv("FLKB_SESSION_TRACE") != nullptr;
   const auto tt0 = Clock::now();
@@ -499,6 +508,10 @@ void Session::submit(const HostImage& img, bool timed) {
     std::copy(tracks_[i].warp, tracks_[i].warp + 4, io[i].w);
     io[i].slot = tracks_[i].slot;
   }
+  // the live records follow the frame on the copy engine, ahead of the graph
+  // (pyramid -> k_track), so the graph holds no copy-engine transitions
+  check_cuda(cudaMemcpyAsync(d_io_, h_io_, kIoHeader + sizeof(lk::TrackIO) * static_cast<size_t>(n),
+                             cudaMemcpyHostToDevice, stream_), "H2D tracks");
   check_cuda(cudaGraphLaunch(graph_exec_[timed ? 1 : 0], stream_), "frame graph");
   count_launches(graph_launches_);
   submitted_ = true;
