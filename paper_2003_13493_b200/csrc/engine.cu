@@ -118,6 +118,32 @@ Geometry Geometry::make(const DetectParams& p, int width, int height) {
   return g;
 }
 
+namespace {
+
+// Multiply-high constants of the per-level cell maps (Level::cmx ...):
+// cx = hi(x * m) + c must equal (x << k) / cell for every coordinate the
+// suppression can produce (3 <= x < w - 3); m = ceil(2^(32+k) / cell), or
+// m = 2^32 - 1, c = 1 where a cell is one level-k pixel. Verified
+// exhaustively; false (-> global-key path) if any level misses.
+bool cell_map(uint32_t& m, uint32_t& c, int k, int cell, int extent) {
+  if (cell < (1 << k)) return false;
+  if (cell == (1 << k)) {
+    m = 0xFFFFFFFFu, c = 1;
+  } else {
+    const uint64_t num = uint64_t{1} << (32 + k);  // k < kMaxLevels: fits
+    const uint64_t q = (num + static_cast<uint64_t>(cell) - 1) / static_cast<uint64_t>(cell);
+    if (q >> 32) return false;
+    m = static_cast<uint32_t>(q), c = 0;
+  }
+  for (int x = 3; x < extent - 3; ++x) {
+    const uint32_t got = static_cast<uint32_t>((static_cast<uint64_t>(x) * m) >> 32) + c;
+    if (got != static_cast<uint32_t>((static_cast<int64_t>(x) << k) / cell)) return false;
+  }
+  return true;
+}
+
+}  // namespace
+
 DeviceBatch::DeviceBatch(const DetectParams& p, int device, int width, int height, int capacity)
     : p_(p), g_(Geometry::make(p, width, height)), device_(device), capacity_(capacity) {
   if (capacity < 1) throw InvalidArgument("batch capacity must be positive");
@@ -141,6 +167,10 @@ DeviceBatch::DeviceBatch(const DetectParams& p, int device, int width, int heigh
   check_cuda(cudaMemset(d_feats_, 0, sizeof(flk_feature) * g_.cells * cap), "memset features");
   check_cuda(cudaMemset(d_counts_, 0, sizeof(int) * cap), "memset counts");
   check_cuda(cudaMemset(d_stats_, 0, sizeof(uint64_t) * 2 * cap), "memset stats");
+  cell_ok_ = true;
+  for (int k = 0; k < g_.levels && cell_ok_; ++k)
+    cell_ok_ = cell_map(cmap_[k][0], cmap_[k][1], k, p_.cell_w, g_.lw[k]) &&
+               cell_map(cmap_[k][2], cmap_[k][3], k, p_.cell_h, g_.lh[k]);
 }
 
 DeviceBatch::~DeviceBatch() {
@@ -322,6 +352,13 @@ void DeviceBatch::run(const uint8_t* frames, size_t fstride, int pitch, int coun
   while (!forced && ctas_of(P) < 148 && P.lv[0].tile_w > 128 && tiles0 < 8) {
     ++tiles0;
     P = fused_geometry(p_, g_, R, tiles0);
+  }
+  if (!cell_ok_) P.key_slots = 0;  // no exact cell maps: global cell keys
+  for (int k = 0; k < g_.levels && cell_ok_; ++k) {
+    P.lv[k].cmx = cmap_[k][0];
+    P.lv[k].ccx = cmap_[k][1];
+    P.lv[k].cmy = cmap_[k][2];
+    P.lv[k].ccy = cmap_[k][3];
   }
   const int smem = fused::smem_layout(P).total;
   if (std::getenv("FLKB_DEBUG_GEOM"))

@@ -135,6 +135,10 @@ class DeviceBatch {
   int fused_tiles0_ = 0;         // level-0 column tiles of that shape (0 = not chosen yet)
   int fused_tile_w_[kMaxLevels] = {};
   int* d_conf_ = nullptr;
+  // per-level cell maps of the fused kernel's shared keys (fused::Level::cmx,
+  // ccx, cmy, ccy), exact for every in-image coordinate when cell_ok_
+  uint32_t cmap_[kMaxLevels][4] = {};
+  bool cell_ok_ = false;
   int last_launches_ = 0;        // kernels enqueued by the last run()
 };
 

@@ -80,6 +80,10 @@ struct Level {
   int tma;              // rows may be fetched with cp.async.bulk
   int nw;               // plane words per row (max over the level's tiles)
   FastDiv div_nw, div_tiles;
+  // grid cell of a level-k pixel: cx = mulhi(x, cmx) + ccx = (x << k) / cell_w,
+  // likewise cy (one IMAD.HI each; the host checks every in-image coordinate;
+  // ccx, ccy are 0 or 1)
+  uint32_t cmx, ccx, cmy, ccy;
 };
 
 struct Params {
@@ -711,7 +715,11 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_detect(const __grid_co
     const int e_hi = T1 > T0 ? scan[kWarps + 2] : 0;
     const int rp = RP;
     const uint32_t kc = static_cast<uint32_t>((1023 + y0) * 1024 + 1023 + x_lo);
-    const uint32_t pk = P.pow2[k];  // level -> level-0 coordinates
+    // cell map constants; the additive parts and the CTA's first cell row
+    // fold into one base slot
+    const uint32_t cmx = L.cmx, cmy = L.cmy;
+    uint32_t* const kbase = skeys + static_cast<int>(L.ccy - static_cast<uint32_t>(cr0)) * P.cols +
+                            static_cast<int>(L.ccx);
     for (int w0 = e_lo; w0 < e_hi; w0 += cap) {
       const bool resident = total <= cap;  // the scoring list is still in place
       const int off = resident ? 0 : w0;
@@ -775,14 +783,14 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_detect(const __grid_co
           if (local_keys) {
             // 32-bit key inside the CTA: score, then smaller y, then smaller x
             // (the level is fixed per CTA), as s << 20 | (1023 - (y - y0)) << 10
-            // | (1023 - (x - x_lo)), built with IMADs; the cell from the
-            // level-0 coordinates with FastDivs (no table loads)
+            // | (1023 - (x - x_lo)), built with IMADs; the cell with one
+            // IMAD.HI per coordinate (no table loads)
             const uint32_t key = mad_fma(static_cast<uint32_t>(s), P.pow2[20],
                                          kc - mad_fma(static_cast<uint32_t>(y), P.pow2[10],
                                                       static_cast<uint32_t>(x)));
-            const int cx = P.div_cw(static_cast<int>(shl_fma(static_cast<uint32_t>(x), pk)));
-            const int cy = P.div_ch(static_cast<int>(shl_fma(static_cast<uint32_t>(y), pk)));
-            atomicMax(skeys + (cy - cr0) * P.cols + cx, key);
+            const uint32_t cx = __umulhi(static_cast<uint32_t>(x), cmx);
+            const uint32_t cy = __umulhi(static_cast<uint32_t>(y), cmy);
+            atomicMax(kbase + mad_fma(cy, static_cast<uint32_t>(P.cols), cx), key);
           } else {
             const int X = x << k, Y = y << k;
             atomicMax(P.keys + static_cast<size_t>(f) * P.cells + P.div_ch(Y) * P.cols + P.div_cw(X),
