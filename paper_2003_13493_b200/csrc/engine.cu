@@ -354,6 +354,12 @@ void DeviceBatch::run(const uint8_t* frames, size_t fstride, int pitch, int coun
     P = fused_geometry(p_, g_, R, tiles0);
   }
   if (!cell_ok_) P.key_slots = 0;  // no exact cell maps: global cell keys
+  // the corner list takes whatever the kMinBlocks-per-SM budget leaves (dense
+  // levels otherwise score a band in several rounds)
+  if (P.list_cap == 0) {
+    const int spare = (kFusedSmemTarget - fused::smem_layout(P).total) / 2 & ~7;
+    if (spare > 0) P.list_cap = fused::list_capacity(P) + spare;
+  }
   for (int k = 0; k < g_.levels && cell_ok_; ++k) {
     P.lv[k].cmx = cmap_[k][0];
     P.lv[k].ccx = cmap_[k][1];

@@ -101,7 +101,7 @@ struct Params {
   int nw_max;     // plane words per row, max over tiles
   int rp;         // score tile pitch (u16)
   int key_slots;  // shared cell-key capacity
-  int list_cap;   // corner-list capacity override (0 = default 6144 entries)
+  int list_cap;   // corner-list capacity (0 = 24 entries per thread)
   uint32_t pow2[32];  // 1 << i, read from the constant bank so shifts can issue as IMAD
   uint32_t emask[8];  // ~0 where bit b of eps is set
   unsigned long long* keys;

@@ -377,3 +377,25 @@ def test_c5_full_batch_4k(orc):
     """BASELINE configs[4]: 3840x2160, l=5, FAST-10 (per-GPU batch of 32)."""
     cfg = dict(epsilon=10, N=10, score_kind="sad_b", l=5, w=1, h=2, n=1)
     _full_batch_check(orc, cfg, 3840, 2160, 32, 2)
+
+
+@pytest.mark.parametrize("l,w,h,cell,size", [
+    (6, 1, 1, None, (600, 300)),       # cells one pixel tall at level 5 (multiplier 2^32-1)
+    (7, 1, 2, None, (640, 512)),       # 32-px cells < 2^6: no exact cell map -> global keys
+    (3, 1, 8, (20, 12), (500, 300)),   # cell sizes not divisible by 2^k: rational multipliers
+    (4, 1, 8, (7, 5), (400, 256)),     # cells smaller than a level-3 pixel -> global keys
+    (2, 1, 8, (3000, 1000), (752, 480)),  # one cell wider and taller than the image
+])
+def test_cell_maps_deep_pyramids_and_odd_cells(orc, l, w, h, cell, size):
+    """The fused kernel's per-level cell maps (one multiply-high per
+    coordinate, host-verified) and their global-key fallback."""
+    img = synth.texture(l + 40, *size)
+    cfg = dict(epsilon=9, N=9, score_kind="sad_b", l=l, w=w, h=h, n=1)
+    if cell:
+        cfg.update(cell_width_px=cell[0], cell_height_px=cell[1])
+    feats, extra = fl.Detector(make_config(cfg)).run(img, stats=True)
+    p = oracle.make_params(**cfg)
+    ref, st = orc.detect(img, p)
+    assert len(feats) > 0
+    assert (feats == ref).all()
+    assert extra["stats"]["nms_comparisons"] == st.comparisons
