@@ -318,18 +318,24 @@ void DeviceBatch::run(const uint8_t* frames, size_t fstride, int pitch, int coun
     // Pick (band rows, column tiles) with the least halo work among the
     // shapes that fit kMinBlocks CTAs per SM: plane words cost ~0.3, mask
     // words ~0.7 per row, plus a fixed per-CTA share (setup, NMS, flush).
+    // Radius 1 keeps to column tiles the compile-time-pitch instance takes
+    // (at most 192 px), unless no such shape fits.
     double best = 1e300;
-    for (int r = std::min(r_max, 40); r >= 12; r -= 4) {
-      for (int t = 1; t <= 8; ++t) {
-        const fused::Params q = fused_geometry(p_, g_, r, t);
-        if (fused::smem_layout(q).total > kFusedSmemTarget) continue;
-        const int n = p_.radius;
-        double cost = 0;
-        for (int k = 0; k < q.levels; ++k)
-          cost += double(q.lv[k].bands) * q.lv[k].tiles_x * q.lv[k].nw *
-                  (0.3 * (r + 2 * n + 6) + 0.7 * (r + 2 * n) + 4.0);
-        if (cost < best) best = cost, R = r, tiles0 = t, P = q;
-        break;  // more tiles at the same r only add column halo
+    const int t_max = p_.radius == 1 ? std::max(8, g_.lw[0] / 176 + 1) : 8;
+    for (int pass = 0; pass < 2 && best == 1e300; ++pass) {
+      for (int r = std::min(r_max, 40); r >= 12; r -= 4) {
+        for (int t = 1; t <= t_max; ++t) {
+          const fused::Params q = fused_geometry(p_, g_, r, t);
+          if (fused::smem_layout(q).total > kFusedSmemTarget) continue;
+          if (pass == 0 && p_.radius == 1 && q.sw != fused::kSw1) continue;
+          const int n = p_.radius;
+          double cost = 0;
+          for (int k = 0; k < q.levels; ++k)
+            cost += double(q.lv[k].bands) * q.lv[k].tiles_x * q.lv[k].nw *
+                    (0.3 * (r + 2 * n + 6) + 0.7 * (r + 2 * n) + 4.0);
+          if (cost < best) best = cost, R = r, tiles0 = t, P = q;
+          break;  // more tiles at the same r only add column halo
+        }
       }
     }
     if (best < 1e300) fused_R_ = R, fused_tiles0_ = tiles0;
