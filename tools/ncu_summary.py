@@ -75,6 +75,19 @@ def main():
             print(f"  pixels in the launch           {npx:14.0f}")
             print(f"  warp instructions / pixel      {wi / npx:10.3f}")
             print(f"  thread instructions / pixel    {wi * tr / npx:10.1f}")
+    print("\n== pipe utilisation (sm__inst_executed_pipe_*.avg.pct_of_peak_sustained_active) and "
+          "stall reasons (warps per issued instruction)")
+    for li, k in enumerate(kernels):
+        pipes = {m.split("pipe_")[1].split(".")[0]: float(v.replace(",", "")) for m, v in k.items()
+                 if m.startswith("sm__inst_executed_pipe_") and m.endswith(".avg.pct_of_peak_sustained_active")
+                 and "subpipe" not in m and "type" not in m and v.strip()}
+        stalls = {m.split("stalled_")[1].split("_per_issue")[0]: float(v.replace(",", ""))
+                  for m, v in k.items()
+                  if m.startswith("smsp__average_warps_issue_stalled_") and v.strip()}
+        top_p = sorted(((v, n) for n, v in pipes.items() if v >= 1.0), reverse=True)
+        top_s = sorted(((v, n) for n, v in stalls.items() if v >= 0.2), reverse=True)
+        print(f"  launch {li} pipes: " + ", ".join(f"{n} {v:.1f}%" for v, n in top_p))
+        print(f"  launch {li} stalls: " + ", ".join(f"{n} {v:.2f}" for v, n in top_s))
     agg = source_lines(a.report)
     tot = sum(v[0] for v in agg.values()) or 1
     ts = sum(v[1] for v in agg.values()) or 1
