@@ -70,9 +70,10 @@ struct Pinned {
   }
 };
 
-// Single-frame pipeline of one detector: pinned staging -> H2D -> kernels ->
-// D2H, replayed as one CUDA graph when no stats are requested (the latency
-// path), or launched stage by stage with events when they are.
+// Single-frame pipeline of one detector: H2D of the frame, then the kernels
+// replayed as one CUDA graph that leaves the feature list in mapped
+// page-locked memory (the latency path), or, when stats or the conformance
+// tally are requested, launched stage by stage with events plus a download.
 class FrameRunner {
  public:
   FrameRunner(const flkb::DetectParams& p, int device, int w, int h)
@@ -164,19 +165,22 @@ class FrameRunner {
   void capture() {
     int* counts = static_cast<int*>(out_.p);
     flk_feature* fv = reinterpret_cast<flk_feature*>(static_cast<char*>(out_.p) + 4 * sizeof(int));
+    // The compaction writes the count and the feature list straight into the
+    // mapped page-locked output (no device-to-host copies to schedule); where
+    // the output is not mapped, the graph downloads them instead.
+    int* dc = nullptr;
+    flk_feature* df = nullptr;
+    if (cudaHostGetDevicePointer(reinterpret_cast<void**>(&dc), counts, 0) != cudaSuccess ||
+        cudaHostGetDevicePointer(reinterpret_cast<void**>(&df), fv, 0) != cudaSuccess) {
+      cudaGetLastError();
+      dc = nullptr;
+      df = nullptr;
+    }
     flkb::check_cuda(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal), "capture");
-    try {
-      // The frame's H2D precedes each replay (its source may change). The
-      // compaction writes the count and the feature list straight into the
-      // mapped page-locked output: no device-to-host copies to schedule.
-      int* dc = nullptr;
-      flk_feature* df = nullptr;
-      flkb::check_cuda(cudaHostGetDevicePointer(reinterpret_cast<void**>(&dc), counts, 0),
-                       "mapped counts");
-      flkb::check_cuda(cudaHostGetDevicePointer(reinterpret_cast<void**>(&df), fv, 0),
-                       "mapped features");
+    try {  // the frame's H2D precedes each replay (its source may change)
       batch_.run(d_in_, static_cast<size_t>(pitch_) * h_, pitch_, 1, false, stream_, nullptr, 0,
                  false, dc, df);
+      if (!dc) batch_.download(0, 1, counts, fv, stream_);
     } catch (...) {
       cudaGraph_t g = nullptr;
       cudaStreamEndCapture(stream_, &g);
