@@ -87,6 +87,20 @@ FLK_API flk_status flkb_batch_device_pyramid(const flkb_batch* batch, int level,
                                              const uint8_t** base, int* width, int* height,
                                              int* row_pitch, size_t* frame_stride);
 
+/* GPU conformance tally (the reference's
+ * oracle::conformance_check, oracle.cpp:240-268, replacing the CPU pass
+ * flk_detector_run makes for a non-NULL conformance, capi.cpp:254-259) of
+ * frames [first, first + count) of the last flkb_batch_run_device: a naive
+ * detector (per-pixel labels, rotation-scan arc test, linear-scan MT, raster
+ * suppression) re-run on the device frames and pyramid, each emitted feature
+ * checked against it. `frames`, `frame_stride`, `row_pitch` as passed to
+ * that run. per_frame (count entries) may be NULL; total receives the sum.
+ * Synchronous on `stream`. */
+FLK_API flk_status flkb_batch_conformance(flkb_batch* batch, const uint8_t* frames,
+                                          size_t frame_stride, int row_pitch, int first,
+                                          int count, flk_conformance* per_frame,
+                                          flk_conformance* total, void* stream);
+
 /* Deterministic synthetic frames written on the device:
  * kind 0 = S1 noise, 1 = S2 texture; frame f gets index first_frame + f. */
 FLK_API flk_status flkb_synth_frames_device(uint8_t* frames, int kind, uint64_t first_frame,

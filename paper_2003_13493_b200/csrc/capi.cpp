@@ -791,6 +791,22 @@ flk_status flkb_batch_download(const flkb_batch* b, int first, int count, int* c
   });
 }
 
+flk_status flkb_batch_conformance(flkb_batch* b, const uint8_t* frames, size_t frame_stride,
+                                  int row_pitch, int first, int count,
+                                  flk_conformance* per_frame, flk_conformance* total,
+                                  void* stream) {
+  if (!b || !frames || !total)
+    return fail(FLK_E_INVALID_ARG, "batch, frames, and total must not be NULL");
+  return guarded([&] {
+    const flkb::Geometry& g = b->batch->geometry();
+    if (row_pitch < g.width || frame_stride < static_cast<size_t>(row_pitch) * g.height)
+      throw flkb::InvalidArgument("row pitch / frame stride smaller than the frame");
+    *total = b->batch->conformance(frames, frame_stride, row_pitch,
+                                   static_cast<cudaStream_t>(stream), first, count, per_frame);
+    return FLK_OK;
+  });
+}
+
 int flkb_batch_frame_capacity(const flkb_batch* b) { return b ? b->batch->geometry().cells : 0; }
 const int* flkb_batch_device_counts(const flkb_batch* b) { return b ? b->batch->device_counts() : nullptr; }
 const flk_feature* flkb_batch_device_features(const flkb_batch* b) {

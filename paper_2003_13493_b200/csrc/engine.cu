@@ -601,26 +601,30 @@ void DeviceBatch::download_responses(int frame, float* out, cudaStream_t s) cons
 }
 
 flk_conformance DeviceBatch::conformance(const uint8_t* frames, size_t fstride, int pitch,
-                                         cudaStream_t s) {
-  (void)fstride;
+                                         cudaStream_t s, int first, int count,
+                                         flk_conformance* per_frame) {
+  if (count < 1 || first < 0 || first + count > capacity_)
+    throw InvalidArgument("conformance range outside the batch");
   DeviceGuard guard(device_);
   size_t total = 0;
   for (int k = 0; k < g_.levels; ++k) total += static_cast<size_t>(g_.lw[k]) * g_.lh[k];
-  // tally[3] | level widths[16] | level heights[16] | map pointers[16]
-  constexpr size_t kTallyBytes = 3 * sizeof(int) + 2 * kMaxLevels * sizeof(int) + 4;
-  if (!d_naive_) d_naive_ = dalloc<float>(total, "conformance maps");
-  if (!d_conf_) d_conf_ = dalloc<int>((kTallyBytes + kMaxLevels * sizeof(float*)) / sizeof(int) + 4,
-                                      "conformance tally");
   struct Tables {
-    int tally[3];
     int lw[kMaxLevels];
     int lh[kMaxLevels];
-    int pad;
     const float* maps[kMaxLevels];
   } t{};
   static_assert(offsetof(Tables, maps) % 8 == 0, "pointer alignment");
+  // scratch: one frame's naive maps (reused frame after frame in stream
+  // order), the level tables, then 3 tally ints per frame
+  if (!d_naive_) d_naive_ = dalloc<float>(total, "conformance maps");
+  const size_t need = sizeof(Tables) + 3 * sizeof(int) * static_cast<size_t>(count);
+  if (need > conf_bytes_) {
+    cudaFree(d_conf_);
+    d_conf_ = nullptr;
+    d_conf_ = dalloc<int>((need + 3) / 4, "conformance tally");
+    conf_bytes_ = need;
+  }
   size_t off = 0;
-  int launched = 0;
   for (int k = 0; k < g_.levels; ++k) {
     t.lw[k] = g_.lw[k];
     t.lh[k] = g_.lh[k];
@@ -628,30 +632,47 @@ flk_conformance DeviceBatch::conformance(const uint8_t* frames, size_t fstride, 
     off += static_cast<size_t>(g_.lw[k]) * g_.lh[k];
   }
   Tables* dt = reinterpret_cast<Tables*>(d_conf_);
+  int* tally = reinterpret_cast<int*>(reinterpret_cast<char*>(d_conf_) + sizeof(Tables));
   check_cuda(cudaMemcpyAsync(dt, &t, sizeof(Tables), cudaMemcpyHostToDevice, s), "upload tables");
-  for (int k = 0; k < g_.levels; ++k) {
-    const uint8_t* img = k == 0 ? frames : d_pyr_ + g_.loff[k];
-    const int ip = k == 0 ? pitch : g_.lpitch[k];
-    dim3 block(32, 8), grid((g_.lw[k] + 31) / 32, (g_.lh[k] + 7) / 8);
-    k_naive_fast<<<grid, block, 0, s>>>(img, ip, g_.lw[k], g_.lh[k], p_.epsilon, p_.arc_length,
-                                        p_.score, const_cast<float*>(t.maps[k]));
-    k_naive_survivors<<<grid, block, 0, s>>>(t.maps[k], g_.lw[k], g_.lh[k], p_.radius,
-                                             dt->tally);
-    launched += 2;
+  check_cuda(cudaMemsetAsync(tally, 0, 3 * sizeof(int) * static_cast<size_t>(count), s), "tally");
+  int launched = 0;
+  for (int i = 0; i < count; ++i) {
+    const int f = first + i;
+    int* tf = tally + 3 * i;
+    for (int k = 0; k < g_.levels; ++k) {
+      const uint8_t* img = k == 0 ? frames + static_cast<size_t>(f) * fstride
+                                  : d_pyr_ + static_cast<size_t>(f) * g_.pyr_frame_bytes + g_.loff[k];
+      const int ip = k == 0 ? pitch : g_.lpitch[k];
+      dim3 block(32, 8), grid((g_.lw[k] + 31) / 32, (g_.lh[k] + 7) / 8);
+      k_naive_fast<<<grid, block, 0, s>>>(img, ip, g_.lw[k], g_.lh[k], p_.epsilon, p_.arc_length,
+                                          p_.score, const_cast<float*>(t.maps[k]));
+      k_naive_survivors<<<grid, block, 0, s>>>(t.maps[k], g_.lw[k], g_.lh[k], p_.radius, tf);
+      launched += 2;
+    }
+    k_conf_features<<<(g_.cells + 127) / 128, 128, 0, s>>>(
+        d_feats_ + static_cast<size_t>(f) * g_.cells, d_counts_ + f, dt->maps, dt->lw, dt->lh,
+        p_.radius, tf);
+    ++launched;
   }
-  k_conf_features<<<(g_.cells + 127) / 128, 128, 0, s>>>(d_feats_, d_counts_, dt->maps, dt->lw,
-                                                         dt->lh, p_.radius, dt->tally);
-  ++launched;
   check_cuda(cudaGetLastError(), "conformance launch");
   count_launches(launched);
-  int host[3] = {0, 0, 0};
-  check_cuda(cudaMemcpyAsync(host, dt->tally, sizeof(host), cudaMemcpyDeviceToHost, s), "tally");
+  std::vector<int> host(3 * static_cast<size_t>(count));
+  check_cuda(cudaMemcpyAsync(host.data(), tally, sizeof(int) * host.size(), cudaMemcpyDeviceToHost,
+                             s), "tally");
   check_cuda(cudaStreamSynchronize(s), "conformance sync");
-  flk_conformance c;
-  c.matched = host[1];
-  c.false_positives = host[2];
-  c.subset_only = host[0] - host[1];
-  return c;
+  // tally = naive survivors, matched, false positives (oracle.cpp:240-268)
+  flk_conformance sum{0, 0, 0};
+  for (int i = 0; i < count; ++i) {
+    flk_conformance c;
+    c.matched = host[3 * i + 1];
+    c.false_positives = host[3 * i + 2];
+    c.subset_only = host[3 * i] - host[3 * i + 1];
+    if (per_frame) per_frame[i] = c;
+    sum.matched += c.matched;
+    sum.subset_only += c.subset_only;
+    sum.false_positives += c.false_positives;
+  }
+  return sum;
 }
 
 namespace {

@@ -95,10 +95,12 @@ class DeviceBatch {
   // Score maps of frame `frame` of the last run, every level, tightly packed
   // floats (the reference's ResponseMap values). Synchronous.
   void download_responses(int frame, float* out, cudaStream_t s) const;
-  // Naive GPU conformance tally (oracle.cpp:240-268 semantics) for frame 0
-  // of the last run; frames pointer/pitch as passed to run().
+  // Naive GPU conformance tally (oracle.cpp:240-268 semantics) of frames
+  // [first, first + count) of the last run (frames / pitch as passed to
+  // run()); per-frame tallies into per_frame (nullable), the sum returned.
   flk_conformance conformance(const uint8_t* frames, size_t frame_stride, int pitch,
-                              cudaStream_t s);
+                              cudaStream_t s, int first = 0, int count = 1,
+                              flk_conformance* per_frame = nullptr);
 
   const Geometry& geometry() const { return g_; }
   const DetectParams& params() const { return p_; }
@@ -135,6 +137,7 @@ class DeviceBatch {
   int fused_tiles0_ = 0;         // level-0 column tiles of that shape (0 = not chosen yet)
   int fused_tile_w_[kMaxLevels] = {};
   int* d_conf_ = nullptr;
+  size_t conf_bytes_ = 0;
   // per-level cell maps of the fused kernel's shared keys (fused::Level::cmx,
   // ccx, cmy, ccy), exact for every in-image coordinate when cell_ok_
   uint32_t cmap_[kMaxLevels][4] = {};

@@ -103,7 +103,7 @@ EXT_SYMBOLS = [
     "flkb_batch_device_counts", "flkb_batch_device_features", "flkb_batch_device_stats",
     "flkb_batch_device_pyramid", "flkb_synth_frames_device", "flkb_kernel_launch_count",
     "flkb_batch_kernels_per_run", "flkb_detector_responses", "flkb_batch_run_device_timed",
-    "flkb_sessions_process", "flkb_features_copy", "flkb_tracks_copy"]
+    "flkb_sessions_process", "flkb_features_copy", "flkb_tracks_copy", "flkb_batch_conformance"]
 
 _lib = None
 _vp = ctypes.c_void_p
@@ -178,6 +178,8 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.flkb_sessions_process.argtypes = [_vp, _vp, ctypes.c_int, _vp, _vp]
     lib.flkb_features_copy.argtypes = [_vp, _vp, ctypes.c_int]
     lib.flkb_tracks_copy.argtypes = [_vp, _vp, ctypes.c_int]
+    lib.flkb_batch_conformance.argtypes = [_vp, _vp, ctypes.c_size_t, ctypes.c_int, ctypes.c_int,
+                                           ctypes.c_int, _vp, _vp, _vp]
     lib.flkb_synth_frames_device.argtypes = [_vp, ctypes.c_int, ctypes.c_uint64, ctypes.c_int,
                                              ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                              ctypes.c_size_t, _vp]
@@ -483,6 +485,18 @@ class DeviceBatch(_Handle):
 
     def device_stats(self) -> int:
         return _lib.flkb_batch_device_stats(self._h)
+
+    def conformance(self, frames_ptr: int, frame_stride: int, row_pitch: int, first: int,
+                    count: int, stream: int = 0):
+        """flkb_batch_conformance: GPU conformance tally of frames [first,
+        first + count) of the last run_device. Returns (total, per_frame)
+        as dicts of matched / subset_only / false_positives."""
+        per = (ConformanceT * count)()
+        tot = ConformanceT()
+        _check(_lib.flkb_batch_conformance(self._h, frames_ptr, frame_stride, row_pitch, first,
+                                           count, per, ctypes.byref(tot), stream or None))
+        as_dict = lambda c: {k: getattr(c, k) for k, _ in ConformanceT._fields_}  # noqa: E731
+        return as_dict(tot), [as_dict(c) for c in per]
 
     def pyramid_level(self, level: int):
         base = _vp()

@@ -205,6 +205,38 @@ def test_conformance_tally_matches_reference_semantics(orc):
     assert len(cells) == len(feats) and (feats["score"] > 0).all()
 
 
+@pytest.mark.parametrize("fuse", ["0", "1"])
+def test_batch_conformance_tally_per_frame(orc, fuse, monkeypatch):
+    """flkb_batch_conformance: the GPU tally of every frame
+    of a device batch equals the reference conformance_check of that frame."""
+    import torch
+    monkeypatch.setenv("FLKB_FUSE_PYR", fuse)
+    W, H, n = 320, 240, 12
+    cfg = dict(epsilon=10, N=9, score_kind="mt", l=3, w=1, h=4, n=2)
+    det = fl.Detector(make_config(cfg))
+    batch = fl.DeviceBatch(det, W, H, n)
+    pitch = 320
+    d = torch.zeros((n, H, pitch), dtype=torch.uint8, device="cuda")
+    fl.synth_frames_device(d.data_ptr(), 0, 7, n, W, H, pitch, pitch * H)
+    batch.run_device(d.data_ptr(), pitch * H, pitch, n)
+    torch.cuda.synchronize()
+    res = batch.results(n)
+    total, per = batch.conformance(d.data_ptr(), pitch * H, pitch, 0, n)
+    p = oracle.make_params(**cfg)
+    for f in range(n):
+        want = orc.conformance(synth.noise(7 + f, W, H), p, res[f])
+        assert (per[f]["matched"], per[f]["subset_only"], per[f]["false_positives"]) == (
+            want.matched, want.subset_only, want.false_positives), f
+        assert per[f]["false_positives"] == 0 and per[f]["matched"] == len(res[f])
+    assert total["matched"] == sum(len(r) for r in res)
+    assert total["subset_only"] == sum(c["subset_only"] for c in per)
+    # a sub-range gives the same per-frame tallies
+    _, sub = batch.conformance(d.data_ptr(), pitch * H, pitch, 5, 3)
+    assert sub == per[5:8]
+    with pytest.raises(fl.InvalidArgument):
+        batch.conformance(d.data_ptr(), pitch * H, pitch, n - 1, 2)
+
+
 def test_errors_through_the_abi():
     det = fl.Detector(fl.Config(l=2, h=16))
     det.run(synth.texture(10, 256, 192))
