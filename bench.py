@@ -506,6 +506,17 @@ def main():
         acc = [a + b for a, b in zip(acc, t3)]
     pyr_us, fused_us, comp_us = (a / reps for a in acc)
     stage_times = (fused_us, pyr_us, comp_us)
+    # the standalone pyramid kernel, reported on its own: the
+    # one-launch plan builds levels 1-2 from level 0 in one k_pyramid_down2
+    # launch (the plan small batches and the tracking session use)
+    saved = os.environ.get("FLKB_FUSE_PYR")
+    os.environ["FLKB_FUSE_PYR"] = "0"
+    pyr_alone_us = sum(batch.run_device_timed(frames.data_ptr(), PITCH * H, PITCH, B, stream)[0]
+                       for _ in range(reps)) / reps
+    if saved is None:
+        del os.environ["FLKB_FUSE_PYR"]
+    else:
+        os.environ["FLKB_FUSE_PYR"] = saved
 
     if rank == 0:
         peak, peak_src = hbm_peak()
@@ -546,6 +557,14 @@ def main():
             "gpu_launches": int(launches),
             "clocks": clocks.summary(),
         }
+        pyr_bytes = level_pixels()  # level 0 read once, levels >= 1 written once
+        pyr_gbs = pyr_bytes * B / (pyr_alone_us / 1e6) / 1e9
+        line["pyramid_roofline"] = {
+            "bound": "hbm", "achieved": pyr_gbs, "peak": peak, "unit": "GB/s",
+            "frac": pyr_gbs / peak, "kernel_us": pyr_alone_us, "bytes_per_frame": pyr_bytes,
+            "kernel": f"flkb::k_pyramid_down2 alone over the {B}-frame batch (levels 1-2 from "
+                      "level 0, one 16x4-block per thread; the one-launch plan's pyramid), "
+                      "CUDA events on its stream"}
         # The path is instruction-issue bound: the same kernels
         # against the SM issue rate (148 SMs x 4 schedulers x 1 warp-instr/clk
         # at the live SM clock), from the committed ncu instruction count.
