@@ -564,11 +564,14 @@ def main():
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "kernel": "flkb::fused::k_detect (FAST + score + NMS + cell keys) over "
-                                   f"a {B}-frame batch: a level-0 launch that also writes pyramid "
-                                   "levels 1-2 from its staged rows, then a launch over levels 1-2; "
-                                   "achieved = the step's algorithmic bytes / the two launches' "
-                                   "summed CUDA-event time",
-                         "kernel_launches_per_step": 2,
+                                   f"a {B}-frame batch, in chunks of frames whose pyramid levels "
+                                   "1-2 fit in a quarter of L2: per chunk a level-0 launch that "
+                                   "also writes levels 1-2 from its staged rows, then a level 1-2 "
+                                   "launch (side stream, overlapping the next chunk's level-0 "
+                                   "launch) that reads them back from L2; achieved = the step's "
+                                   "algorithmic bytes / the CUDA-event time from the first to the "
+                                   "last of these launches",
+                         "kernel_launches_per_step": int(launches) // args.steps - 1,
                          "kernel_us_per_step": fused_us,
                          "kernel_share_of_step": fused_us / (fused_us + pyr_us + comp_us),
                          "other_kernels_us": {"pyramid": pyr_us, "compact": comp_us},
@@ -597,8 +600,8 @@ def main():
             line["issue_roofline"] = {
                 "bound": "issue", "unit": "G warp-instr/s", "achieved": kern_i, "peak": peak_i,
                 "frac": kern_i / peak_i, "warp_instr_per_frame": wipf,
-                "note": "k_detect warp instructions per frame (ncu) x frames per launch / the "
-                        "two launches' CUDA-event time, against 148 SMs x 4 issue slots x SM clock",
+                "note": "k_detect warp instructions per frame (ncu) x frames per step / the "
+                        "step's k_detect CUDA-event time, against 148 SMs x 4 issue slots x SM clock",
                 "source": wsrc}
         if not args.no_extras and world == 1:
             line["other_configs"] = other_configs(local)

@@ -183,6 +183,8 @@ DeviceBatch::~DeviceBatch() {
   cudaFree(d_feats_);
   cudaFree(d_counts_);
   cudaFree(d_stats_);
+  for (cudaEvent_t e : evs_) cudaEventDestroy(e);
+  if (side_) cudaStreamDestroy(side_);
   cudaFree(d_naive_);
   cudaFree(d_conf_);
   if (cur >= 0) cudaSetDevice(cur);
@@ -421,19 +423,23 @@ void DeviceBatch::run(const uint8_t* frames, size_t fstride, int pitch, int coun
   }
   if (stats) check_cuda(cudaMemsetAsync(st, 0, sizeof(uint64_t) * 2 * count, s), "memset stats");
   int launched = 0;
-  for (int k = 0; k < g_.levels; ++k) {
-    fused::Level& L = P.lv[k];
-    L.img = k == 0 ? frames : pyr + g_.loff[k];
-    L.pitch = k == 0 ? pitch : g_.lpitch[k];
-    L.fstride = k == 0 ? fstride : g_.pyr_frame_bytes;
-    L.tma = (reinterpret_cast<uintptr_t>(L.img) % 16 == 0) && L.pitch % 16 == 0 &&
-            L.fstride % 16 == 0;
-    if (k > 0 && k < 3) P.pyr_img[k] = pyr + g_.loff[k];
-  }
-  P.keys = keys;
-  P.stats = stats ? st : nullptr;
-  // detection of levels [kb, ke) in one launch
-  auto detect = [&](int kb, int ke, int pyr_levels) {
+  // frame pointers of the frames [c0, c0 + n) of this call
+  auto bind = [&](int c0) {
+    for (int k = 0; k < g_.levels; ++k) {
+      fused::Level& L = P.lv[k];
+      L.img = k == 0 ? frames + static_cast<size_t>(c0) * fstride
+                     : pyr + static_cast<size_t>(c0) * g_.pyr_frame_bytes + g_.loff[k];
+      L.pitch = k == 0 ? pitch : g_.lpitch[k];
+      L.fstride = k == 0 ? fstride : g_.pyr_frame_bytes;
+      L.tma = (reinterpret_cast<uintptr_t>(L.img) % 16 == 0) && L.pitch % 16 == 0 &&
+              L.fstride % 16 == 0;
+      if (k > 0 && k < 3) P.pyr_img[k] = const_cast<uint8_t*>(L.img);
+    }
+    P.keys = keys + static_cast<size_t>(c0) * g_.cells;
+    P.stats = stats ? st + 2 * static_cast<size_t>(c0) : nullptr;
+  };
+  // detection of levels [kb, ke) of n frames in one launch
+  auto detect = [&](int kb, int ke, int pyr_levels, int n, cudaStream_t ls) {
     P.k_begin = kb;
     P.k_end = ke;
     P.pyr_levels = pyr_levels;
@@ -442,20 +448,64 @@ void DeviceBatch::run(const uint8_t* frames, size_t fstride, int pitch, int coun
       P.lv[k].cta0 = ctas;
       ctas += P.lv[k].bands * P.lv[k].tiles_x;
     }
-    kern<<<dim3(ctas, count), fused::kThreads, smem, s>>>(P);
+    kern<<<dim3(ctas, n), fused::kThreads, smem, ls>>>(P);
     ++launched;
   };
+  // Two-launch plan in chunks of frames whose pyramid levels 1-2 fit in L2:
+  // the level 1-2 launch of a chunk reads what the level-0 launch just wrote
+  // from L2 instead of HBM.
+  // (equal chunks of at most 32 MiB of levels 1-2: a quarter of the L2)
+  int chunk = count;
   if (fuse_pyr) {
-    detect(0, 1, fuse_pyr);
+    size_t b12 = 0;
+    for (int k = 1; k <= fuse_pyr; ++k) b12 += static_cast<size_t>(g_.lpitch[k]) * g_.lh[k];
+    const size_t nchunks = (static_cast<size_t>(count) * b12 + (32u << 20) - 1) / (32u << 20);
+    chunk = static_cast<int>((count + nchunks - 1) / std::max<size_t>(nchunks, 1));
+  }
+  if (const char* e = std::getenv("FLKB_PYR_CHUNK")) chunk = std::max(1, std::atoi(e));
+  if (fuse_pyr) {
     if (times) check_cuda(cudaEventRecord(ev[1], s), "cudaEventRecord");
-    launched += enqueue_pyramid(frames, fstride, pitch, count, s, first, fuse_pyr + 1);
     if (times) check_cuda(cudaEventRecord(ev[2], s), "cudaEventRecord");
-    detect(1, g_.levels, 0);
+    // chunk i's level 1-2 launch runs on a side stream, overlapping chunk
+    // i+1's level-0 launch (their tails fill each other's idle SMs)
+    const bool overlap = chunk < count;
+    cudaStream_t s1 = s;
+    if (overlap) {
+      if (!side_) check_cuda(cudaStreamCreateWithFlags(&side_, cudaStreamNonBlocking), "side stream");
+      const size_t need = 2 * static_cast<size_t>((count + chunk - 1) / chunk) + 1;
+      while (evs_.size() < need) {
+        cudaEvent_t e;
+        check_cuda(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+        evs_.push_back(e);
+      }
+      s1 = side_;
+      check_cuda(cudaEventRecord(evs_[0], s), "fork");
+      check_cuda(cudaStreamWaitEvent(side_, evs_[0], 0), "fork wait");
+    }
+    int ei = 1;
+    for (int c0 = 0; c0 < count; c0 += chunk) {
+      const int n = std::min(chunk, count - c0);
+      bind(c0);
+      detect(0, 1, fuse_pyr, n, s);
+      launched += enqueue_pyramid(frames + static_cast<size_t>(c0) * fstride, fstride, pitch, n, s,
+                                  first + c0, fuse_pyr + 1);
+      if (overlap) {
+        check_cuda(cudaEventRecord(evs_[ei], s), "chunk level 0 done");
+        check_cuda(cudaStreamWaitEvent(side_, evs_[ei], 0), "chunk wait");
+        ++ei;
+      }
+      detect(1, g_.levels, 0, n, s1);
+    }
+    if (overlap) {
+      check_cuda(cudaEventRecord(evs_[ei], side_), "join");
+      check_cuda(cudaStreamWaitEvent(s, evs_[ei], 0), "join wait");
+    }
   } else {
+    bind(0);
     if (!pyramid_ready) launched += enqueue_pyramid(frames, fstride, pitch, count, s, first);
     if (times) check_cuda(cudaEventRecord(ev[1], s), "cudaEventRecord");
     if (times) check_cuda(cudaEventRecord(ev[2], s), "cudaEventRecord");
-    detect(0, g_.levels, 0);
+    detect(0, g_.levels, 0, count, s);
   }
   if (times) check_cuda(cudaEventRecord(ev[3], s), "cudaEventRecord");
   k_compact<<<count, 256, 0, s>>>(keys, g_.cols, g_.cells, feats, counts);
@@ -475,7 +525,7 @@ void DeviceBatch::run(const uint8_t* frames, size_t fstride, int pitch, int coun
     // the two-launch plan, pyramid levels 1-2): its time is crf_us;
     // pyramid_us is the separate downsampling launches; nms_us is the cell
     // compaction.
-    if (fuse_pyr) {
+    if (fuse_pyr) {  // the pyramid is made inside the fused launches
       times->pyramid_us = b * 1e3;
       times->crf_us = (a + c) * 1e3;
     } else {

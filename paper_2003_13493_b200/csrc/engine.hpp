@@ -17,6 +17,7 @@
 #include <cstdint>
 #include <memory>
 #include <string>
+#include <vector>
 
 #include "../../include/fastlk.h"
 #include "common.hpp"
@@ -142,7 +143,9 @@ class DeviceBatch {
   // ccx, cmy, ccy), exact for every in-image coordinate when cell_ok_
   uint32_t cmap_[kMaxLevels][4] = {};
   bool cell_ok_ = false;
-  int last_launches_ = 0;        // kernels enqueued by the last run()
+  int last_launches_ = 0;
+  cudaStream_t side_ = nullptr;      // chunked two-launch plan: level 1-2 launches
+  std::vector<cudaEvent_t> evs_;     // its fork / per-chunk / join events        // kernels enqueued by the last run()
 };
 
 // Device synthetic generator, bit-identical to tests/synth.py.
