@@ -575,7 +575,8 @@ def main():
                          "kernel_us_per_step": fused_us,
                          "kernel_share_of_step": fused_us / (fused_us + pyr_us + comp_us),
                          "other_kernels_us": {"pyramid": pyr_us, "compact": comp_us},
-                         "bytes_per_frame": bytes_frame, "bytes_per_launch": bytes_frame * B,
+                         "bytes_per_frame": bytes_frame, "bytes_per_step": bytes_frame * B,
+                         "traffic_over_algorithmic": (traffic / (bytes_frame * B)) if traffic else None,
                          "step_achieved_gbs": step_achieved, "peak_source": peak_src,
                          "traffic_source": traffic_src},
             "gpu_launches": int(launches),
