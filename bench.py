@@ -100,7 +100,23 @@ class ClockSampler:
         self.device = device
         self.samples = []
         self._stop = threading.Event()
+        self._ready = threading.Event()  # the first sample is in (or sampling failed)
         self._t = None
+        self._nvml = None
+
+    def _sample(self):
+        if self._nvml is not None:
+            nv, hnd, mx, bits = self._nvml
+            sm = nv.nvmlDeviceGetClockInfo(hnd, nv.NVML_CLOCK_SM)
+            r = nv.nvmlDeviceGetCurrentClocksEventReasons(hnd)
+            self.samples.append([str(sm), str(mx)] +
+                                ["Active" if r & b else "Not Active" for b in bits])
+            return
+        out = subprocess.run(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                              "--format=csv,noheader,nounits"], capture_output=True,
+                             text=True, timeout=5).stdout.strip()
+        if out:
+            self.samples.append([x.strip() for x in out.split(",")])
 
     def _run(self):
         try:  # NVML directly: ~1 ms per sample instead of a process per sample
@@ -110,38 +126,38 @@ class ClockSampler:
             mx = nv.nvmlDeviceGetMaxClockInfo(hnd, nv.NVML_CLOCK_SM)
             bits = [nv.nvmlClocksEventReasonHwSlowdown, nv.nvmlClocksEventReasonHwThermalSlowdown,
                     nv.nvmlClocksEventReasonSwThermalSlowdown, nv.nvmlClocksEventReasonSwPowerCap]
-            while not self._stop.is_set():
-                sm = nv.nvmlDeviceGetClockInfo(hnd, nv.NVML_CLOCK_SM)
-                r = nv.nvmlDeviceGetCurrentClocksEventReasons(hnd)
-                self.samples.append([str(sm), str(mx)] +
-                                    ["Active" if r & b else "Not Active" for b in bits])
-                self._stop.wait(0.05)
-            return
+            self._nvml = (nv, hnd, mx, bits)
         except Exception:
-            self.samples.clear()
+            self._nvml = None
+        period = 0.05 if self._nvml is not None else 0.2
         while not self._stop.is_set():
             try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
-                                      "--format=csv,noheader,nounits"], capture_output=True,
-                                     text=True, timeout=5).stdout.strip()
-                if out:
-                    self.samples.append([x.strip() for x in out.split(",")])
+                self._sample()
             except Exception:
+                self._ready.set()
                 return
-            self._stop.wait(0.2)
+            self._ready.set()
+            self._stop.wait(period)
+        self._ready.set()
 
     def __enter__(self):
         self._t = threading.Thread(target=self._run, daemon=True)
         self._t.start()
+        self._ready.wait(timeout=15)  # sampling is live when the timed region starts
         return self
 
     def __exit__(self, *a):
         self._stop.set()
         self._t.join(timeout=10)
+        if len(self.samples) < 2:  # a short region: one more sample right at its end
+            try:
+                self._sample()
+            except Exception:
+                pass
 
     def summary(self):
         if not self.samples:
-            return None
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
         sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
         mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
