@@ -399,6 +399,29 @@ def test_c4_full_batch_4096(orc, fuse, monkeypatch):
     assert sum(len(f) for f in res) > 4096 * 300
 
 
+def test_chunked_two_launch_plan_is_invariant(monkeypatch):
+    """The two-launch plan's chunking (level 1-2 launches on a side stream
+    overlapping the next chunk's level-0 launch) never changes a result: every
+    chunk size gives the unchunked feature lists."""
+    import torch
+    W, H, n = 752, 480, 1200
+    cfg = dict(epsilon=10, N=9, score_kind="sad_b", l=3, w=1, h=8, n=1)
+    det = fl.Detector(make_config(cfg))
+    pitch = 768
+    d = torch.empty((n, H, pitch), dtype=torch.uint8, device="cuda")
+    fl.synth_frames_device(d.data_ptr(), 1, 77, n, W, H, pitch, pitch * H)
+    monkeypatch.setenv("FLKB_FUSE_PYR", "1")
+    out = {}
+    for chunk in ("1200", "1", "7", "256", "599"):
+        monkeypatch.setenv("FLKB_PYR_CHUNK", chunk)
+        batch = fl.DeviceBatch(det, W, H, n)
+        batch.run_device(d.data_ptr(), pitch * H, pitch, n)
+        torch.cuda.synchronize()
+        out[chunk] = np.concatenate(batch.results(n))
+    for chunk, f in out.items():
+        assert len(f) == len(out["1200"]) and (f == out["1200"]).all(), chunk
+
+
 def test_c3_full_batch_256_16px_cells(orc):
     """BASELINE configs[2]: 256 frames of 1920x1080, l=4, FAST-12, 16x16 cells."""
     cfg = dict(epsilon=10, N=12, score_kind="sad_b", l=4, w=1, h=2, n=1)
