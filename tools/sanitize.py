@@ -1,8 +1,9 @@
 #!/usr/bin/env python
 """Small representative runs for compute-sanitizer (memcheck / racecheck /
 synccheck / initcheck): the fused detector (both pyramid plans, radius 1-3,
-every score kind, unaligned pitch, multi-round corner lists), the staged
-kernels, the conformance kernel and a short tracking session. Checks parity
+every score kind, unaligned pitch, multi-round corner lists, a chunked device
+batch), the staged kernels, the conformance kernels and a short tracking
+session. Checks parity
 with the oracle on each so a sanitizer run is also a correctness run.
 
     compute-sanitizer --tool racecheck python tools/sanitize.py
@@ -45,6 +46,24 @@ def main():
     feats = fl.Detector(fl.Config(**cfg)).run(img)
     assert (feats == orc.detect(img, oracle.make_params(**cfg))[0]).all()
     del os.environ["FLKB_LIST_CAP"]
+    # a device batch in the chunked two-launch plan (side-stream level 1-2
+    # launches) and its GPU conformance tally
+    import torch
+    os.environ["FLKB_FUSE_PYR"] = "1"
+    os.environ["FLKB_PYR_CHUNK"] = "3"
+    W, H, n = 256, 160, 8
+    cfg = dict(epsilon=10, N=9, score_kind="sad_b", l=3, w=1, h=8, n=1)
+    batch = fl.DeviceBatch(fl.Detector(fl.Config(**cfg)), W, H, n)
+    d = torch.empty((n, H, W), dtype=torch.uint8, device="cuda")
+    fl.synth_frames_device(d.data_ptr(), 1, 40, n, W, H, W, W * H)
+    batch.run_device(d.data_ptr(), W * H, W, n)
+    torch.cuda.synchronize()
+    res = batch.results(n)
+    for f in (0, n - 1):
+        assert (res[f] == orc.detect(synth.texture(40 + f, W, H), oracle.make_params(**cfg))[0]).all()
+    total, _ = batch.conformance(d.data_ptr(), W * H, W, 0, n)
+    assert total["false_positives"] == 0 and total["matched"] == sum(len(r) for r in res)
+    del os.environ["FLKB_PYR_CHUNK"]
     frames = sessions.drifting_sequence(3, 192, 128)
     scfg = dict(epsilon=10, N=9, score_kind="sad_b", l=2, w=1, h=16, n=1, target_count=12,
                 redetect_ratio=0.5, param_mode="full", max_iterations=30, convergence_epsilon=0.01)
