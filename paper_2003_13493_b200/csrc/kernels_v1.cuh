@@ -238,7 +238,12 @@ __global__ void __launch_bounds__(256) k_compact(unsigned long long* __restrict_
     __syncthreads();
     if (key) {
       const int slot = base + warp_base[warp] + __popc(ballot & ((1u << lane) - 1u));
-      out[slot] = unpack_key(key, i % cols, i / cols);
+      // three 8-byte stores per record (the list may be mapped host memory)
+      const flk_feature ft = unpack_key(key, i % cols, i / cols);
+      uint2* o = reinterpret_cast<uint2*>(out + slot);
+      o[0] = make_uint2(static_cast<uint32_t>(ft.x), static_cast<uint32_t>(ft.y));
+      o[1] = make_uint2(__float_as_uint(ft.score), static_cast<uint32_t>(ft.level));
+      o[2] = make_uint2(static_cast<uint32_t>(ft.cell_x), static_cast<uint32_t>(ft.cell_y));
     }
     base += warp_base[32];
     __syncthreads();
