@@ -292,13 +292,12 @@ __global__ void __launch_bounds__(256) k_track(Levels lv, const int* __restrict_
     if (k == finest) finest_converged = level_converged;
   }
   if (!aborted && !finest_converged) status = 4;  // MAX_ITERATIONS
-  if (tid == 0) {
-    io_out[t].status = status;
-    io_out[t].iters = iters;
-    io_out[t].w[0] = tx0;
-    io_out[t].w[1] = ty0;
-    io_out[t].w[2] = gain;
-    io_out[t].w[3] = offset;
+  if (tid == 0) {  // three 16-byte stores into the mapped record
+    static_assert(sizeof(TrackIO) == 48 && offsetof(TrackIO, slot) == 32, "TrackIO layout");
+    double2* o = reinterpret_cast<double2*>(io_out + t);
+    o[0] = make_double2(tx0, ty0);
+    o[1] = make_double2(gain, offset);
+    reinterpret_cast<int4*>(io_out + t)[2] = make_int4(slot, status, iters, 0);
   }
 }
 
