@@ -448,7 +448,21 @@ void DeviceBatch::run(const uint8_t* frames, size_t fstride, int pitch, int coun
       P.lv[k].cta0 = ctas;
       ctas += P.lv[k].bands * P.lv[k].tiles_x;
     }
-    kern<<<dim3(ctas, n), fused::kThreads, smem, ls>>>(P);
+    if (P.pdl_wait) {  // overlap the pyramid kernel (and this launch's latency)
+      cudaLaunchConfig_t lc{};
+      lc.gridDim = dim3(ctas, n);
+      lc.blockDim = dim3(fused::kThreads);
+      lc.dynamicSmemBytes = smem;
+      lc.stream = ls;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      at[0].val.programmaticStreamSerializationAllowed = 1;
+      lc.attrs = at;
+      lc.numAttrs = 1;
+      check_cuda(cudaLaunchKernelEx(&lc, kern, P), "fused launch (programmatic)");
+    } else {
+      kern<<<dim3(ctas, n), fused::kThreads, smem, ls>>>(P);
+    }
     ++launched;
   };
   // Two-launch plan in chunks of frames whose pyramid levels 1-2 fit in L2:
@@ -502,10 +516,15 @@ void DeviceBatch::run(const uint8_t* frames, size_t fstride, int pitch, int coun
     }
   } else {
     bind(0);
-    if (!pyramid_ready) launched += enqueue_pyramid(frames, fstride, pitch, count, s, first);
+    int pyr_launches = 0;
+    if (!pyramid_ready) pyr_launches = enqueue_pyramid(frames, fstride, pitch, count, s, first);
+    launched += pyr_launches;
     if (times) check_cuda(cudaEventRecord(ev[1], s), "cudaEventRecord");
     if (times) check_cuda(cudaEventRecord(ev[2], s), "cudaEventRecord");
+    static const bool pdl = !(std::getenv("FLKB_PDL") && std::atoi(std::getenv("FLKB_PDL")) == 0);
+    P.pdl_wait = pdl && pyr_launches > 0 && !times;
     detect(0, g_.levels, 0, count, s);
+    P.pdl_wait = 0;
   }
   if (times) check_cuda(cudaEventRecord(ev[3], s), "cudaEventRecord");
   k_compact<<<count, 256, 0, s>>>(keys, g_.cols, g_.cells, feats, counts);

@@ -93,7 +93,10 @@ struct Params {
   // Pyramid levels 1..pyr_levels (<= 2) written by the level-0 CTAs from their
   // staged rows (needs R % 4 == 0 and 16-px aligned column tiles); 0 = none.
   int pyr_levels;
-  uint8_t* pyr_img[3];  // frame 0, row 0 of levels 1, 2 (index = level)
+  uint8_t* pyr_img[3];
+  // launched as a programmatic dependent of the pyramid kernel: CTAs of
+  // levels >= 1 wait for it (griddepcontrol.wait), level-0 CTAs start at once
+  int pdl_wait;  // frame 0, row 0 of levels 1, 2 (index = level)
   int eps, radius, R;
   int cell_w, cell_h, cols, cells;
   FastDiv div_cw, div_ch;
@@ -364,6 +367,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_detect(const __grid_co
   const bool local_keys = slots <= P.key_slots;
 
   // --- 1. stage the rows [ya, yb), columns [max(bx0,0), ...) of this tile
+  if (k > 0 && P.pdl_wait) asm volatile("griddepcontrol.wait;" ::: "memory");
   const uint8_t* frame = L.img + f * L.fstride;
   const int gx0 = max(bx0, 0);
   const int sx0 = gx0 - bx0;  // multiple of 16

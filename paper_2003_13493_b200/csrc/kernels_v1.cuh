@@ -23,6 +23,9 @@ __global__ void __launch_bounds__(256) k_pyramid_down(const uint8_t* __restrict_
                                                       int spitch, size_t sfs,
                                                       uint8_t* __restrict__ dst, int dpitch,
                                                       size_t dfs, int wd, int hd, int vec_ok) {
+  // a programmatic dependent (the fused detector) may launch now; its CTAs
+  // that read the pyramid wait for this grid with griddepcontrol.wait
+  asm volatile("griddepcontrol.launch_dependents;");
   const int f = blockIdx.z;
   const int y = blockIdx.y * blockDim.y + threadIdx.y;
   const int x8 = (blockIdx.x * blockDim.x + threadIdx.x) * 8;
@@ -52,6 +55,7 @@ __global__ void __launch_bounds__(256) k_pyramid_down2(const uint8_t* __restrict
                                                        uint8_t* __restrict__ d1, int p1,
                                                        uint8_t* __restrict__ d2, int p2, size_t dfs,
                                                        int w1, int h1, int w2, int h2, int vec_ok) {
+  asm volatile("griddepcontrol.launch_dependents;");  // see k_pyramid_down
   const int f = blockIdx.z;
   const int ty = blockIdx.y * blockDim.y + threadIdx.y;     // level-k row pair, level-(k+1) row
   const int x8 = (blockIdx.x * blockDim.x + threadIdx.x) * 8;  // first level-k column
