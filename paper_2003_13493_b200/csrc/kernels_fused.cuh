@@ -532,7 +532,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_detect(const __grid_co
         load_planes(pl, ph, q);
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
-          if (ring_dy(i) != dy) continue;
+          if (ring_dy(i) != dy || i == 12) continue;
           const int dx = ring_dx(i);
           uint32_t s[8];
 #pragma unroll
@@ -541,6 +541,13 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_detect(const __grid_co
           bk[i] = sliced_less(hi, s);
         }
       }
+      // ring positions 4 (3,0) and 12 (-3,0) are antipodal in one row:
+      // I(p-3) + eps < I(p) is bright_4 at p-3, I(p) + eps < I(p-3) is dark_4
+      // at p-3 (the saturations of sat(c -+ eps) drop out of both forms), so
+      // position 12 is position 4 shifted by three bit lanes -- exact on the
+      // owned bits [3, 29), since bright_4 / dark_4 hold on bits [0, 29)
+      dk[12] = shl_fma(bk[4], P.pow2[3]);
+      bk[12] = shl_fma(dk[4], P.pow2[3]);
       uint32_t corner = sliced_arc<N>(dk) | sliced_arc<N>(bk);
       // owned bits [3, 29) that fall inside the FAST columns
       const int xb = bx0 + kOwn * j;
