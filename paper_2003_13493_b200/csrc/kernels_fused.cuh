@@ -507,23 +507,19 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_detect(const __grid_co
         q[0] = u.x; q[1] = u.y; q[2] = u.z; q[3] = u.w;
         q[4] = v.x; q[5] = v.y; q[6] = v.z; q[7] = v.w;
       };
-      uint32_t c[8], lo[8], hi[8];
+      // c - eps and c + eps mod 256; the lanes where they wrap (borrow br:
+      // c < eps, carry cy: c + eps > 255) can have no dark resp. bright ring
+      // pixel under sat(c -+ eps), so they are cleared once from the arcs
+      // rather than by clamping 16 threshold planes
+      uint32_t c[8], lo[8], hi[8], br = 0, cy = 0;
       load_planes(pl + 3 * stride, ph + 3 * stride, c);
-      {
-        uint32_t br = 0, cy = 0;
 #pragma unroll
-        for (int b = 0; b < 8; ++b) {
-          // plain C so ptxas can take E[b] straight from the constant bank
-          lo[b] = c[b] ^ E[b] ^ br;
-          br = (~c[b] & E[b]) | (~c[b] & br) | (E[b] & br);
-          hi[b] = c[b] ^ E[b] ^ cy;
-          cy = (c[b] & E[b]) | (c[b] & cy) | (E[b] & cy);
-        }
-#pragma unroll
-        for (int b = 0; b < 8; ++b) {
-          lo[b] &= ~br;  // c - eps < 0  -> 0
-          hi[b] |= cy;   // c + eps > 255 -> 255
-        }
+      for (int b = 0; b < 8; ++b) {
+        // plain C so ptxas can take E[b] straight from the constant bank
+        lo[b] = c[b] ^ E[b] ^ br;
+        br = (~c[b] & E[b]) | (~c[b] & br) | (E[b] & br);
+        hi[b] = c[b] ^ E[b] ^ cy;
+        cy = (c[b] & E[b]) | (c[b] & cy) | (E[b] & cy);
       }
       uint32_t dk[16], bk[16];
 #pragma unroll
@@ -545,10 +541,11 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_detect(const __grid_co
       // I(p-3) + eps < I(p) is bright_4 at p-3, I(p) + eps < I(p-3) is dark_4
       // at p-3 (the saturations of sat(c -+ eps) drop out of both forms), so
       // position 12 is position 4 shifted by three bit lanes -- exact on the
-      // owned bits [3, 29), since bright_4 / dark_4 hold on bits [0, 29)
-      dk[12] = shl_fma(bk[4], P.pow2[3]);
-      bk[12] = shl_fma(dk[4], P.pow2[3]);
-      uint32_t corner = sliced_arc<N>(dk) | sliced_arc<N>(bk);
+      // owned bits [3, 29), since bright_4 / dark_4 hold on bits [0, 29) once
+      // their wrapped-threshold lanes are cleared
+      dk[12] = shl_fma(bk[4] & ~cy, P.pow2[3]);
+      bk[12] = shl_fma(dk[4] & ~br, P.pow2[3]);
+      uint32_t corner = (sliced_arc<N>(dk) & ~br) | (sliced_arc<N>(bk) & ~cy);
       // owned bits [3, 29) that fall inside the FAST columns
       const int xb = bx0 + kOwn * j;
       const int lo_b = max(3, cx_lo - xb), hi_b = min(29, cx_hi - xb);
