@@ -39,6 +39,29 @@ FLK_API flk_status flkb_detector_run_batch(flk_detector* detector,
                                            const flk_image* const* images, int n,
                                            flk_features** outs, flk_frame_stats* stats);
 
+/* Many host frames over several GPUs of one host, in one call: frames are
+ * split into contiguous shards, shard r = frames [r*n/ndev, ...) runs on
+ * devices[r] through its own two-slot pipeline (device workspace, streams,
+ * page-locked staging) driven by its own host thread; results land in
+ * disjoint slots of outs (outs[i] = frame i's features, caller frees each).
+ * Frames are independent, so there is no exchange between the GPUs (SURVEY
+ * 8(e)); the output is identical to flkb_detector_run_batch for any device
+ * list, including one device listed several times. The reference's only
+ * parallelism is parallel_chunks' host threads (parallel.hpp:33-52) under
+ * the same determinism contract. On an error every out is NULL. */
+FLK_API flk_status flkb_detector_run_batch_multi(flk_detector* detector, const int* devices,
+                                                 int ndev, const flk_image* const* images, int n,
+                                                 flk_features** outs);
+
+/* Launch-plan overrides for tests and tuning tools (the engine reads no
+ * environment variables): keys "band_rows", "tiles" (0 = shape search),
+ * "fuse_pyramid" (-1 auto, 0 one-launch plan, 1 two-launch plan),
+ * "pyramid_chunk" (frames, 0 = auto), "pdl" (0/1), "list_cap" (corner-list
+ * entries, 0 = auto), "debug_geom" (0/1). Results never depend on the plan.
+ * Setting a detector's plan drops its cached device workspaces; batches take
+ * the detector's plan at creation. Unknown key: FLK_E_CONFIG. */
+FLK_API flk_status flkb_detector_set_plan(flk_detector* detector, const char* key, int value);
+
 /* ---------------------------------------------------------- device batches */
 
 /* A device-resident workspace for up to `capacity` frames of width x height
@@ -48,6 +71,8 @@ typedef struct flkb_batch flkb_batch;
 FLK_API flk_status flkb_batch_create(flk_detector* detector, int width, int height,
                                      int capacity, flkb_batch** out);
 FLK_API void flkb_batch_destroy(flkb_batch* batch);
+/* flkb_detector_set_plan for one batch. */
+FLK_API flk_status flkb_batch_set_plan(flkb_batch* batch, const char* key, int value);
 
 /* Detects on `count` device frames: frame f row y starts at
  * frames + f*frame_stride + y*row_pitch. Asynchronous on `stream`; results
@@ -69,6 +94,16 @@ FLK_API flk_status flkb_batch_run_device_timed(flkb_batch* batch, const uint8_t*
 FLK_API flk_status flkb_batch_run_host(flkb_batch* batch, const uint8_t* frames,
                                        size_t frame_stride, int row_pitch, int count,
                                        void* stream);
+
+/* Host frames in, host feature lists out, one pipelined call: chunks of
+ * frames alternate over two streams so each chunk's H2D overlaps the previous
+ * chunk's kernels and its feature download overlaps the next chunk's kernels.
+ * counts / features as for flkb_batch_download(batch, 0, count, ...) (either
+ * may be NULL, not both; pinned host memory for overlap). Asynchronous on
+ * `stream`. */
+FLK_API flk_status flkb_batch_detect_host(flkb_batch* batch, const uint8_t* frames,
+                                          size_t frame_stride, int row_pitch, int count,
+                                          int* counts, flk_feature* features, void* stream);
 
 /* Copies per-frame counts and the compact feature lists to the host.
  * features is count * flkb_batch_frame_capacity() entries; frame f's list
@@ -113,6 +148,12 @@ FLK_API flk_status flkb_synth_frames_device(uint8_t* frames, int kind, uint64_t 
  * point for parity tests; subject to the detector's frame-size latch. */
 FLK_API flk_status flkb_detector_responses(flk_detector* detector, const flk_image* image,
                                            float* out);
+/* The same maps as the production fused kernel (k_detect) computes them: each
+ * CTA writes the scores of its own rows and columns from its shared-memory
+ * score tile (a diagnostic dump; pixels that are no corner read 0). Equal to
+ * flkb_detector_responses by construction of the parity tests. */
+FLK_API flk_status flkb_detector_fused_responses(flk_detector* detector, const flk_image* image,
+                                                 float* out);
 
 /* ------------------------------------------------------- many sessions */
 
@@ -133,6 +174,11 @@ FLK_API flk_status flkb_sessions_process(flk_session* const* sessions,
  * return the number copied; NULL handles copy nothing. */
 FLK_API int flkb_features_copy(const flk_features* features, flk_feature* out, int cap);
 FLK_API int flkb_tracks_copy(const flk_tracks* tracks, flk_track_info* out, int cap);
+
+/* Test hook: the tracker's device hypot (glibc's algorithm, so convergence
+ * and divergence tests match the reference's std::hypot, lk.cpp:267,319) on
+ * n host pairs. Synchronous. */
+FLK_API flk_status flkb_debug_hypot(const double* x, const double* y, double* out, int n);
 
 /* Number of CUDA kernels this library has launched in the process (graph
  * replays count every kernel node). */

@@ -416,8 +416,11 @@ class Reference(_Base):
             raise ValueError(f"reference track_feature rejected ({rc})")
         return res
 
-    def bench(self, frames: np.ndarray, config: dict, mode: int, workers: int):
-        """Seconds to run flk_detector_run over every frame (see ref_harness.cpp)."""
+    def bench(self, frames: np.ndarray, config: dict, mode: int, workers: int,
+              collect: bool = False, stages: bool = False):
+        """Seconds to run flk_detector_run over every frame (see ref_harness.cpp).
+        Returns (seconds, total features[, (counts, features[n, cap])][, stage
+        microseconds summed over frames: pyramid, crf, nms])."""
         frames = np.ascontiguousarray(frames, dtype=np.uint8)
         n, h, w = frames.shape
         keys = [k.encode() for k in config]
@@ -425,11 +428,43 @@ class Reference(_Base):
         karr = (ctypes.c_char_p * len(keys))(*keys)
         varr = (ctypes.c_char_p * len(vals))(*vals)
         feats = ctypes.c_longlong()
+        cap = 0
+        out = counts = None
+        if collect:
+            p = make_params(**{k: config[k] for k in ("epsilon", "N", "score_kind", "l", "w", "h",
+                                                       "n") if k in config})
+            cap = _grid_cap(w, h, p)
+            out = np.zeros((n, cap), FEATURE_DTYPE)
+            counts = np.zeros(n, np.int32)
+        st = (ctypes.c_double * 3)() if stages else None
         secs = self.lib.refh_bench(_ptr(frames, _u8p), n, w, h, karr, varr, len(keys),
-                                   mode, workers, ctypes.byref(feats))
+                                   mode, workers, ctypes.byref(feats),
+                                   out.ctypes.data_as(ctypes.c_void_p) if collect else None, cap,
+                                   counts.ctypes.data_as(ctypes.c_void_p) if collect else None,
+                                   st)
         if secs < 0:
             raise RuntimeError(f"reference bench failed ({secs})")
-        return secs, feats.value
+        res = [secs, feats.value]
+        if collect:
+            res.append((counts, out))
+        if stages:
+            res.append(tuple(st))
+        return tuple(res)
+
+    def detect_batch(self, frames: np.ndarray, p: Params, workers: int | None = None):
+        """refh_detect over every frame, frame-parallel: (counts[n], feats[n, cap])."""
+        frames = np.ascontiguousarray(frames, dtype=np.uint8)
+        n, h, w = frames.shape
+        cap = _grid_cap(w, h, p)
+        out = np.zeros((n, cap), FEATURE_DTYPE)
+        counts = np.zeros(n, np.int32)
+        rc = self.lib.refh_detect_batch(_ptr(frames, _u8p), n, w, h, ctypes.byref(p),
+                                        workers or os.cpu_count() or 1,
+                                        out.ctypes.data_as(ctypes.c_void_p), cap,
+                                        counts.ctypes.data_as(ctypes.c_void_p))
+        if rc:
+            raise ValueError(f"reference detect_batch rejected ({rc})")
+        return counts, out
 
 
 def build(ref: bool = True) -> None:

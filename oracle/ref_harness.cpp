@@ -5,6 +5,7 @@
 // the reference bit for bit, and it times the reference's public C API for
 // bench.py's reference arm. No reference source is copied here; this file
 // only calls the reference headers' public functions.
+#include <algorithm>
 #include <atomic>
 #include <chrono>
 #include <cstring>
@@ -235,11 +236,17 @@ __attribute__((visibility("default"))) int refh_conformance(const uint8_t* img, 
 // `workers` threads, each with its own threads=1 detector, pulling frames
 // from a shared counter. Frame images are created before the clock starts.
 // Returns seconds, or a negative value on error; *features_out sums counts.
+// Optional outputs (NULL = not collected): frame i's feature list at
+// out + i*cap with its count in counts[i] (whole-batch parity against the
+// GPU), and the sums over frames of flk_frame_stats' pyramid_us / crf_us /
+// nms_us in stage_us[0..2] (the reference's per-stage split, frontend.cpp:38-57).
 __attribute__((visibility("default"))) double refh_bench(const uint8_t* frames, int n, int w,
                                                          int h, const char* const* keys,
                                                          const char* const* values, int nkv,
                                                          int mode, int workers,
-                                                         long long* features_out) {
+                                                         long long* features_out,
+                                                         flk_feature* out, int cap, int* counts,
+                                                         double* stage_us) {
   std::vector<flk_image*> imgs(static_cast<size_t>(n), nullptr);
   for (int i = 0; i < n; ++i)
     if (flk_image_create(w, h, frames + static_cast<size_t>(i) * w * h, &imgs[i]) != FLK_OK)
@@ -257,17 +264,26 @@ __attribute__((visibility("default"))) double refh_bench(const uint8_t* frames, 
   };
   std::atomic<long long> feats{0};
   std::atomic<int> failed{0};
+  std::vector<flk_frame_stats> fstats(stage_us ? static_cast<size_t>(n) : 0);
+  auto one = [&](flk_detector* det, int i) {
+    flk_features* f = nullptr;
+    if (flk_detector_run(det, imgs[i], &f, stage_us ? &fstats[i] : nullptr, nullptr) != FLK_OK)
+      failed = 1;
+    const int c = flk_features_count(f);
+    feats += c;
+    if (out && counts) {
+      counts[i] = c;
+      for (int j = 0; j < c && j < cap; ++j)
+        flk_features_get(f, j, out + static_cast<size_t>(i) * cap + j);
+    }
+    flk_features_destroy(f);
+  };
   double secs = 0.0;
   if (mode == 0) {
     flk_detector* det = make_det("0");
     if (!det) return -2.0;
     auto t0 = std::chrono::steady_clock::now();
-    for (int i = 0; i < n; ++i) {
-      flk_features* f = nullptr;
-      if (flk_detector_run(det, imgs[i], &f, nullptr, nullptr) != FLK_OK) failed = 1;
-      feats += flk_features_count(f);
-      flk_features_destroy(f);
-    }
+    for (int i = 0; i < n; ++i) one(det, i);
     secs = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     flk_detector_destroy(det);
   } else {
@@ -279,12 +295,7 @@ __attribute__((visibility("default"))) double refh_bench(const uint8_t* frames, 
     std::vector<std::thread> pool;
     for (int t = 0; t < workers; ++t)
       pool.emplace_back([&, t] {
-        for (int i; (i = next.fetch_add(1)) < n;) {
-          flk_features* f = nullptr;
-          if (flk_detector_run(dets[t], imgs[i], &f, nullptr, nullptr) != FLK_OK) failed = 1;
-          feats += flk_features_count(f);
-          flk_features_destroy(f);
-        }
+        for (int i; (i = next.fetch_add(1)) < n;) one(dets[t], i);
       });
     for (auto& th : pool) th.join();
     secs = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
@@ -292,7 +303,37 @@ __attribute__((visibility("default"))) double refh_bench(const uint8_t* frames, 
   }
   for (auto* im : imgs) flk_image_destroy(im);
   if (features_out) *features_out = feats.load();
+  if (stage_us) {
+    stage_us[0] = stage_us[1] = stage_us[2] = 0.0;
+    for (const auto& st : fstats) {
+      stage_us[0] += st.pyramid_us;
+      stage_us[1] += st.crf_us;
+      stage_us[2] += st.nms_us;
+    }
+  }
   return failed ? -3.0 : secs;
+}
+
+// refh_detect over n frames, `workers` threads pulling frames from a shared
+// counter (each frame's detection single-threaded): frame i's features at
+// out + i*cap, its count in counts[i]. Whole-batch parity for configurations
+// the public API cannot express (the cell-size override of refh_detect).
+__attribute__((visibility("default"))) int refh_detect_batch(const uint8_t* frames, int n, int w,
+                                                             int h, const orc_params* p,
+                                                             int workers, orc_feature* out,
+                                                             int cap, int* counts) {
+  std::atomic<int> next{0}, rc{ORC_OK};
+  std::vector<std::thread> pool;
+  for (int t = 0; t < std::max(1, workers); ++t)
+    pool.emplace_back([&] {
+      for (int i; (i = next.fetch_add(1)) < n;) {
+        const int r = refh_detect(frames + static_cast<size_t>(i) * w * h, w, h, p,
+                                  out + static_cast<size_t>(i) * cap, cap, counts + i, nullptr, 1);
+        if (r != ORC_OK) rc = r;
+      }
+    });
+  for (auto& th : pool) th.join();
+  return rc.load();
 }
 
 }  // extern "C"

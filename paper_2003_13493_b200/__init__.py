@@ -7,9 +7,9 @@ holds its build script and a thin Python mirror of the reference interface.
 from .fastlk import (  # noqa: F401
     FEATURE_DTYPE, TRACK_DTYPE, Config, ConfigError, Detector, Session, sessions_process,
     DeviceBatch, DimensionMismatch, FastlkError, Image, InternalError, InvalidArgument, IoError,
-    device_count, kernel_launch_count, load_library, status_name, synth_frames_device, version)
+    debug_hypot, device_count, kernel_launch_count, load_library, status_name, synth_frames_device, version)
 
 __all__ = ["FEATURE_DTYPE", "TRACK_DTYPE", "Session", "sessions_process", "Config", "ConfigError", "Detector", "DeviceBatch",
            "DimensionMismatch", "FastlkError", "Image", "InternalError", "InvalidArgument",
-           "IoError", "device_count", "kernel_launch_count", "load_library", "status_name",
+           "IoError", "debug_hypot", "device_count", "kernel_launch_count", "load_library", "status_name",
            "synth_frames_device", "version"]

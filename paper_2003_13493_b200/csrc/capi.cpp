@@ -10,10 +10,12 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <exception>
 #include <cstring>
 #include <memory>
 #include <new>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/fastlk.h"
@@ -138,11 +140,23 @@ class FrameRunner {
     if (conf) *conf = batch_.conformance(d_in_, static_cast<size_t>(pitch_) * h_, pitch_, stream_);
   }
 
-  // Staged run that keeps the score maps, for flkb_detector_responses.
-  void responses(const flkb::HostImage& img, float* out) {
+  // Staged run that keeps the score maps, for flkb_detector_responses; with
+  // `fused`, the production kernel's own scores (its diagnostic dump).
+  void responses(const flkb::HostImage& img, float* out, bool fused = false) {
     flkb::DeviceGuard guard(device_);
     copy_in(img);
-    batch_.run_staged(d_in_, static_cast<size_t>(pitch_) * h_, pitch_, 1, false, stream_);
+    if (fused) {
+      batch_.set_dump_scores(true);
+      try {
+        batch_.run(d_in_, static_cast<size_t>(pitch_) * h_, pitch_, 1, false, stream_);
+      } catch (...) {
+        batch_.set_dump_scores(false);
+        throw;
+      }
+      batch_.set_dump_scores(false);
+    } else {
+      batch_.run_staged(d_in_, static_cast<size_t>(pitch_) * h_, pitch_, 1, false, stream_);
+    }
     batch_.download_responses(0, out, stream_);
   }
 
@@ -236,6 +250,17 @@ struct flk_detector {
   int first_height = 0;
   std::unique_ptr<FrameRunner> runner;
   std::unique_ptr<BatchPipeline> pipeline;  // flkb_detector_run_batch
+  // flkb_detector_run_batch_multi: one pipeline per listed device (position i
+  // of the list runs on multi_devices[i])
+  std::vector<int> multi_devices;
+  std::vector<std::unique_ptr<BatchPipeline>> multi;
+  // drops every cached device workspace (device or launch-plan change)
+  void reset_workspaces() {
+    runner.reset();
+    pipeline.reset();
+    multi.clear();
+    multi_devices.clear();
+  }
 };
 struct flk_session {
   std::unique_ptr<flkb::Session> session;
@@ -304,7 +329,12 @@ class BatchPipeline {
 
   void run(const flk_image* const* images, int n, flk_features** outs) {
     flkb::DeviceGuard guard(device_);
-    for (auto& sl : slots_) sl.first = -1;
+    // a previous call that failed mid-pipeline may have left copies into or
+    // out of the staging buffers in flight: finish them before reuse
+    for (auto& sl : slots_) {
+      flkb::check_cuda(cudaStreamSynchronize(sl.s), "batch slot sync");
+      sl.first = -1;
+    }
     int si = 0;
     for (int c0 = 0; c0 < n; c0 += kChunk, si ^= 1) {
       Slot& sl = slots_[si];
@@ -361,6 +391,39 @@ class BatchPipeline {
   size_t fs_ = 0;
   Slot slots_[2];
 };
+
+// Argument checks shared by the host-batch entry points: NULL images, the
+// detector's first-frame size latch (capi.cpp:240-250) applied to every
+// frame; every out slot starts NULL.
+void latch_batch(flk_detector* detector, const flk_image* const* images, int n,
+                 flk_features** outs) {
+  if (n < 0) throw flkb::InvalidArgument("negative frame count");
+  for (int i = 0; i < n; ++i) {
+    if (!images[i]) throw flkb::InvalidArgument("NULL image in batch");
+    outs[i] = nullptr;
+  }
+  if (n == 0) return;
+  if (detector->first_width == 0) {
+    detector->first_width = images[0]->img.width;
+    detector->first_height = images[0]->img.height;
+  }
+  for (int i = 0; i < n; ++i)
+    if (images[i]->img.width != detector->first_width ||
+        images[i]->img.height != detector->first_height)
+      throw flkb::DimensionMismatch("batch frame " + std::to_string(i) + " is " +
+                                    std::to_string(images[i]->img.width) + "x" +
+                                    std::to_string(images[i]->img.height) + ", detector expects " +
+                                    std::to_string(detector->first_width) + "x" +
+                                    std::to_string(detector->first_height));
+}
+
+// Contiguous, balanced frame shards: shard r of `parts` covers
+// [start, start + count) (the first total % parts shards get one extra).
+void shard_range(int total, int r, int parts, int* start, int* count) {
+  const int base = total / parts, extra = total % parts;
+  *start = r * base + std::min(r, extra);
+  *count = base + (r < extra ? 1 : 0);
+}
 
 }  // namespace
 
@@ -563,6 +626,12 @@ flk_status flkb_sessions_process(flk_session* const* sessions, const flk_image* 
     out_tracks[i] = nullptr;
     if (!sessions[i] || !images[i]) return fail(FLK_E_INVALID_ARG, "NULL session or image");
   }
+  {  // one frame per session and call: a repeated handle would stage twice
+    std::vector<const flk_session*> seen(sessions, sessions + n);
+    std::sort(seen.begin(), seen.end());
+    if (std::adjacent_find(seen.begin(), seen.end()) != seen.end())
+      return fail(FLK_E_INVALID_ARG, "the same session appears more than once");
+  }
   int submitted = 0;
   flk_status first = FLK_OK;
   std::string first_msg;
@@ -633,7 +702,7 @@ flk_status flkb_detector_set_device(flk_detector* detector, int device) {
   return guarded([&] {
     if (device < 0 || device >= flkb_device_count())
       throw flkb::InvalidArgument("no CUDA device " + std::to_string(device));
-    if (device != detector->device) detector->runner.reset();
+    if (device != detector->device) detector->reset_workspaces();
     detector->device = device;
     return FLK_OK;
   });
@@ -644,30 +713,19 @@ flk_status flkb_detector_run_batch(flk_detector* detector, const flk_image* cons
   if (!detector || !images || !outs)
     return fail(FLK_E_INVALID_ARG, "detector, images, and outs must not be NULL");
   return guarded([&] {
-    if (n < 0) throw flkb::InvalidArgument("negative frame count");
-    for (int i = 0; i < n; ++i) {
-      if (!images[i]) throw flkb::InvalidArgument("NULL image in batch");
-      outs[i] = nullptr;
-    }
+    latch_batch(detector, images, n, outs);
     if (n == 0) return FLK_OK;
-    const int W = images[0]->img.width, H = images[0]->img.height;
-    if (detector->first_width == 0) {
-      detector->first_width = W;
-      detector->first_height = H;
-    }
-    for (int i = 0; i < n; ++i)
-      if (images[i]->img.width != detector->first_width ||
-          images[i]->img.height != detector->first_height)
-        throw flkb::DimensionMismatch("batch frame " + std::to_string(i) + " is " +
-                                      std::to_string(images[i]->img.width) + "x" +
-                                      std::to_string(images[i]->img.height) + ", detector expects " +
-                                      std::to_string(detector->first_width) + "x" +
-                                      std::to_string(detector->first_height));
     if (stats) {
       // counters need the per-frame stats kernels; run frame by frame
       for (int i = 0; i < n; ++i) {
         flk_status s = flk_detector_run(detector, images[i], &outs[i], &stats[i], nullptr);
-        if (s != FLK_OK) return s;
+        if (s != FLK_OK) {  // like the pipelined path: no handle survives a failure
+          for (int j = 0; j < i; ++j) {
+            flk_features_destroy(outs[j]);
+            outs[j] = nullptr;
+          }
+          return s;
+        }
       }
       return FLK_OK;
     }
@@ -684,6 +742,82 @@ flk_status flkb_detector_run_batch(flk_detector* detector, const flk_image* cons
       }
       throw;
     }
+    return FLK_OK;
+  });
+}
+
+flk_status flkb_detector_run_batch_multi(flk_detector* detector, const int* devices, int ndev,
+                                         const flk_image* const* images, int n,
+                                         flk_features** outs) {
+  if (!detector || !devices || !images || !outs)
+    return fail(FLK_E_INVALID_ARG, "detector, devices, images, and outs must not be NULL");
+  return guarded([&] {
+    if (ndev < 1) throw flkb::InvalidArgument("at least one device is needed");
+    const int avail = flkb_device_count();
+    if (avail == 0) current_device();  // throws: no CUDA device, no CPU fallback
+    for (int i = 0; i < ndev; ++i)
+      if (devices[i] < 0 || devices[i] >= avail)
+        throw flkb::InvalidArgument("no CUDA device " + std::to_string(devices[i]));
+    latch_batch(detector, images, n, outs);
+    if (n == 0) return FLK_OK;
+    // one pipeline (device workspace, streams, pinned staging) per listed
+    // device, kept across calls while the list stays the same
+    const std::vector<int> want(devices, devices + ndev);
+    if (want != detector->multi_devices) {
+      detector->multi.clear();
+      detector->multi_devices = want;
+    }
+    while (static_cast<int>(detector->multi.size()) < ndev) {
+      const int d = want[detector->multi.size()];
+      detector->multi.push_back(std::make_unique<BatchPipeline>(
+          detector->params, d, detector->first_width, detector->first_height));
+    }
+    // one host thread per device over its contiguous frame shard; the shards'
+    // results land in disjoint slots of outs, so no merge is needed
+    std::vector<std::exception_ptr> errs(static_cast<size_t>(ndev));
+    auto work = [&](int r) {
+      int start = 0, count = 0;
+      shard_range(n, r, ndev, &start, &count);
+      if (count == 0) return;
+      try {
+        detector->multi[static_cast<size_t>(r)]->run(images + start, count, outs + start);
+      } catch (...) {
+        errs[static_cast<size_t>(r)] = std::current_exception();
+      }
+    };
+    std::vector<std::thread> pool;
+    for (int r = 1; r < ndev; ++r) pool.emplace_back(work, r);
+    work(0);
+    for (auto& t : pool) t.join();
+    for (auto& e : errs) {
+      if (!e) continue;
+      for (int i = 0; i < n; ++i) {
+        flk_features_destroy(outs[i]);
+        outs[i] = nullptr;
+      }
+      std::rethrow_exception(e);
+    }
+    return FLK_OK;
+  });
+}
+
+flk_status flkb_detector_set_plan(flk_detector* detector, const char* key, int value) {
+  if (!detector || !key) return fail(FLK_E_INVALID_ARG, "detector and key must not be NULL");
+  return guarded([&] {
+    if (!detector->params.plan.set(key, value))
+      throw flkb::ConfigError(std::string("unknown launch-plan key '") + key + "'");
+    detector->reset_workspaces();
+    return FLK_OK;
+  });
+}
+
+flk_status flkb_batch_set_plan(flkb_batch* b, const char* key, int value) {
+  if (!b || !key) return fail(FLK_E_INVALID_ARG, "batch and key must not be NULL");
+  return guarded([&] {
+    flkb::LaunchPlan plan = b->batch->params().plan;
+    if (!plan.set(key, value))
+      throw flkb::ConfigError(std::string("unknown launch-plan key '") + key + "'");
+    b->batch->set_plan(plan);
     return FLK_OK;
   });
 }
@@ -728,56 +862,83 @@ flk_status flkb_batch_run_device_timed(flkb_batch* b, const uint8_t* frames, siz
   });
 }
 
+namespace {
+
+// Chunked H2D -> detect (-> D2H) over the batch's two side streams, joined
+// back into the caller's stream: chunk c's H2D overlaps chunk c-1's kernels,
+// and with host outputs chunk c's feature download overlaps chunk c+1's
+// kernels (H2D and D2H use separate copy engines).
+void run_host_chunks(flkb_batch* b, const uint8_t* frames, size_t frame_stride, int row_pitch,
+                     int count, cudaStream_t user, int* counts, flk_feature* features) {
+  flkb::DeviceBatch& db = *b->batch;
+  const flkb::Geometry& g = db.geometry();
+  if (count < 1 || count > db.capacity()) throw flkb::InvalidArgument("count outside the batch");
+  if (row_pitch < g.width || frame_stride < static_cast<size_t>(row_pitch) * g.height)
+    throw flkb::InvalidArgument("host frame layout smaller than the frame size");
+  flkb::DeviceGuard guard(b->device);
+  if (!b->d_in) {
+    // frames stay densely packed when the width is already 16-B aligned, so
+    // the H2D copy is one linear transfer
+    b->in_pitch = static_cast<int>(round16(static_cast<size_t>(g.width)));
+    b->in_stride = static_cast<size_t>(b->in_pitch) * g.height;
+    flkb::check_cuda(cudaMalloc(&b->d_in, b->in_stride * db.capacity() + 16), "batch input");
+    for (auto& s : b->side) flkb::check_cuda(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "stream");
+    for (auto& e : b->ev) flkb::check_cuda(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+  }
+  flkb::check_cuda(cudaEventRecord(b->ev[0], user), "event");
+  for (auto s : b->side) flkb::check_cuda(cudaStreamWaitEvent(s, b->ev[0], 0), "wait");
+  const int chunk = std::max(1, std::min(count, 256));
+  const size_t cells = static_cast<size_t>(g.cells);
+  int si = 0;
+  for (int c0 = 0; c0 < count; c0 += chunk, si ^= 1) {
+    const int cnt = std::min(chunk, count - c0);
+    cudaStream_t s = b->side[si];
+    uint8_t* dst = b->d_in + static_cast<size_t>(c0) * b->in_stride;
+    const uint8_t* src = frames + static_cast<size_t>(c0) * frame_stride;
+    if (row_pitch == b->in_pitch && frame_stride == b->in_stride) {
+      flkb::check_cuda(cudaMemcpyAsync(dst, src, b->in_stride * cnt, cudaMemcpyHostToDevice, s),
+                       "H2D frames");
+    } else if (frame_stride == static_cast<size_t>(row_pitch) * g.height) {
+      flkb::check_cuda(cudaMemcpy2DAsync(dst, b->in_pitch, src, row_pitch, g.width,
+                                         static_cast<size_t>(g.height) * cnt,
+                                         cudaMemcpyHostToDevice, s), "H2D frames");
+    } else {
+      for (int j = 0; j < cnt; ++j)
+        flkb::check_cuda(cudaMemcpy2DAsync(dst + j * b->in_stride, b->in_pitch,
+                                           src + j * frame_stride, row_pitch, g.width, g.height,
+                                           cudaMemcpyHostToDevice, s), "H2D frame");
+    }
+    db.run(dst, b->in_stride, b->in_pitch, cnt, false, s, nullptr, c0);
+    if (counts || features)
+      db.download(c0, cnt, counts ? counts + c0 : nullptr,
+                  features ? features + static_cast<size_t>(c0) * cells : nullptr, s);
+  }
+  flkb::check_cuda(cudaEventRecord(b->ev[1], b->side[0]), "event");
+  flkb::check_cuda(cudaEventRecord(b->ev[2], b->side[1]), "event");
+  flkb::check_cuda(cudaStreamWaitEvent(user, b->ev[1], 0), "wait");
+  flkb::check_cuda(cudaStreamWaitEvent(user, b->ev[2], 0), "wait");
+}
+
+}  // namespace
+
 flk_status flkb_batch_run_host(flkb_batch* b, const uint8_t* frames, size_t frame_stride,
                                int row_pitch, int count, void* stream) {
   if (!b || !frames) return fail(FLK_E_INVALID_ARG, "batch and frames must not be NULL");
   return guarded([&] {
-    flkb::DeviceBatch& db = *b->batch;
-    const flkb::Geometry& g = db.geometry();
-    if (count < 1 || count > db.capacity()) throw flkb::InvalidArgument("count outside the batch");
-    if (row_pitch < g.width || frame_stride < static_cast<size_t>(row_pitch) * g.height)
-      throw flkb::InvalidArgument("host frame layout smaller than the frame size");
-    flkb::DeviceGuard guard(b->device);
-    if (!b->d_in) {
-      // frames stay densely packed when the width is already 16-B aligned, so
-      // the H2D copy is one linear transfer
-      b->in_pitch = static_cast<int>(round16(static_cast<size_t>(g.width)));
-      b->in_stride = static_cast<size_t>(b->in_pitch) * g.height;
-      flkb::check_cuda(cudaMalloc(&b->d_in, b->in_stride * db.capacity() + 16), "batch input");
-      for (auto& s : b->side) flkb::check_cuda(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "stream");
-      for (auto& e : b->ev) flkb::check_cuda(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
-    }
-    cudaStream_t user = static_cast<cudaStream_t>(stream);
-    // Chunked copy/compute overlap on two side streams, joined back into the
-    // caller's stream: chunk c's H2D overlaps chunk c-1's kernels.
-    flkb::check_cuda(cudaEventRecord(b->ev[0], user), "event");
-    for (auto s : b->side) flkb::check_cuda(cudaStreamWaitEvent(s, b->ev[0], 0), "wait");
-    const int chunk = std::max(1, std::min(count, 256));
-    int si = 0;
-    for (int c0 = 0; c0 < count; c0 += chunk, si ^= 1) {
-      const int cnt = std::min(chunk, count - c0);
-      cudaStream_t s = b->side[si];
-      uint8_t* dst = b->d_in + static_cast<size_t>(c0) * b->in_stride;
-      const uint8_t* src = frames + static_cast<size_t>(c0) * frame_stride;
-      if (row_pitch == b->in_pitch && frame_stride == b->in_stride) {
-        flkb::check_cuda(cudaMemcpyAsync(dst, src, b->in_stride * cnt, cudaMemcpyHostToDevice, s),
-                         "H2D frames");
-      } else if (frame_stride == static_cast<size_t>(row_pitch) * g.height) {
-        flkb::check_cuda(cudaMemcpy2DAsync(dst, b->in_pitch, src, row_pitch, g.width,
-                                           static_cast<size_t>(g.height) * cnt,
-                                           cudaMemcpyHostToDevice, s), "H2D frames");
-      } else {
-        for (int j = 0; j < cnt; ++j)
-          flkb::check_cuda(cudaMemcpy2DAsync(dst + j * b->in_stride, b->in_pitch,
-                                             src + j * frame_stride, row_pitch, g.width, g.height,
-                                             cudaMemcpyHostToDevice, s), "H2D frame");
-      }
-      db.run(dst, b->in_stride, b->in_pitch, cnt, false, s, nullptr, c0);
-    }
-    flkb::check_cuda(cudaEventRecord(b->ev[1], b->side[0]), "event");
-    flkb::check_cuda(cudaEventRecord(b->ev[2], b->side[1]), "event");
-    flkb::check_cuda(cudaStreamWaitEvent(user, b->ev[1], 0), "wait");
-    flkb::check_cuda(cudaStreamWaitEvent(user, b->ev[2], 0), "wait");
+    run_host_chunks(b, frames, frame_stride, row_pitch, count, static_cast<cudaStream_t>(stream),
+                    nullptr, nullptr);
+    return FLK_OK;
+  });
+}
+
+flk_status flkb_batch_detect_host(flkb_batch* b, const uint8_t* frames, size_t frame_stride,
+                                  int row_pitch, int count, int* counts, flk_feature* features,
+                                  void* stream) {
+  if (!b || !frames || (!counts && !features))
+    return fail(FLK_E_INVALID_ARG, "batch, frames, and an output must not be NULL");
+  return guarded([&] {
+    run_host_chunks(b, frames, frame_stride, row_pitch, count, static_cast<cudaStream_t>(stream),
+                    counts, features);
     return FLK_OK;
   });
 }
@@ -845,7 +1006,9 @@ flk_status flkb_synth_frames_device(uint8_t* frames, int kind, uint64_t first_fr
   });
 }
 
-flk_status flkb_detector_responses(flk_detector* detector, const flk_image* image, float* out) {
+namespace {
+flk_status detector_responses(flk_detector* detector, const flk_image* image, float* out,
+                              bool fused) {
   if (!detector || !image || !out)
     return fail(FLK_E_INVALID_ARG, "detector, image, and out must not be NULL");
   return guarded([&] {
@@ -859,7 +1022,26 @@ flk_status flkb_detector_responses(flk_detector* detector, const flk_image* imag
     if (!detector->runner)
       detector->runner = std::make_unique<FrameRunner>(detector->params, detector->device,
                                                        image->img.width, image->img.height);
-    detector->runner->responses(image->img, out);
+    detector->runner->responses(image->img, out, fused);
+    return FLK_OK;
+  });
+}
+}  // namespace
+
+flk_status flkb_detector_responses(flk_detector* detector, const flk_image* image, float* out) {
+  return detector_responses(detector, image, out, false);
+}
+
+flk_status flkb_detector_fused_responses(flk_detector* detector, const flk_image* image,
+                                         float* out) {
+  return detector_responses(detector, image, out, true);
+}
+
+flk_status flkb_debug_hypot(const double* x, const double* y, double* out, int n) {
+  if (!x || !y || !out) return fail(FLK_E_INVALID_ARG, "x, y, and out must not be NULL");
+  return guarded([&] {
+    current_device();
+    flkb::lk::debug_hypot(x, y, out, n);
     return FLK_OK;
   });
 }

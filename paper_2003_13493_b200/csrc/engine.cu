@@ -73,6 +73,18 @@ DeviceGuard::~DeviceGuard() {
   if (cudaGetDevice(&cur) == cudaSuccess && cur != prev_ && prev_ >= 0) cudaSetDevice(prev_);
 }
 
+bool LaunchPlan::set(const std::string& key, int value) {
+  if (key == "band_rows") band_rows = value < 0 ? 0 : value;
+  else if (key == "tiles") tiles = value < 0 ? 0 : value;
+  else if (key == "fuse_pyramid") fuse_pyramid = value < 0 ? -1 : (value != 0);
+  else if (key == "pyramid_chunk") pyramid_chunk = value < 0 ? 0 : value;
+  else if (key == "pdl") pdl = value != 0;
+  else if (key == "list_cap") list_cap = value <= 0 ? 0 : std::max(256, value);
+  else if (key == "debug_geom") debug_geom = value != 0;
+  else return false;
+  return true;
+}
+
 DetectParams DetectParams::from(const Config& c) {
   DetectParams p;
   p.epsilon = c.epsilon;
@@ -252,7 +264,7 @@ fused::Params fused_geometry(const DetectParams& p, const Geometry& g, int R, in
   P.key_slots = slots <= 4096 ? slots : 0;
   for (int i = 0; i < 32; ++i) P.pow2[i] = 1u << i;
   for (int b = 0; b < 8; ++b) P.emask[b] = ((p.epsilon >> b) & 1) ? 0xFFFFFFFFu : 0u;
-  if (const char* e = std::getenv("FLKB_LIST_CAP")) P.list_cap = std::max(256, std::atoi(e));
+  P.list_cap = p.plan.list_cap;
   return P;
 }
 
@@ -306,12 +318,13 @@ void DeviceBatch::run(const uint8_t* frames, size_t fstride, int pitch, int coun
   DeviceGuard guard(device_);
   int R = fused_R_;
   const int r_min = 8;
-  const char* forced = std::getenv("FLKB_BAND_ROWS");  // tuning override
+  const LaunchPlan& plan = p_.plan;
+  const bool forced = plan.band_rows > 0;  // tuning / test override
   // u16 corner-list entries hold the band row in 6 bits: R + 2 radius <= 64
   const int r_max = std::max(4, (64 - 2 * p_.radius) & ~3);
-  if (forced) R = std::min(r_max, std::max(4, std::atoi(forced)));
-  const char* forced_tiles = std::getenv("FLKB_TILES");  // tuning override
-  int tiles0 = forced_tiles ? std::max(1, std::atoi(forced_tiles)) : 1;
+  if (forced) R = std::min(r_max, std::max(4, plan.band_rows));
+  const bool forced_tiles = plan.tiles > 0;  // tuning / test override
+  int tiles0 = forced_tiles ? plan.tiles : 1;
   fused::Params P = fused_geometry(p_, g_, R, tiles0);
   if (!forced && !forced_tiles && fused_tiles0_ > 0) {
     R = fused_R_, tiles0 = fused_tiles0_;
@@ -374,8 +387,18 @@ void DeviceBatch::run(const uint8_t* frames, size_t fstride, int pitch, int coun
     P.lv[k].cmy = cmap_[k][2];
     P.lv[k].ccy = cmap_[k][3];
   }
+  if (dump_scores_) {  // the staged maps' layout: level k at pitch lpitch[k], levels back to back
+    size_t off = 0;
+    for (int k = 0; k < g_.levels; ++k) {
+      P.lv[k].dbg_off = off;
+      P.lv[k].dbg_pitch = g_.lpitch[k];
+      off += static_cast<size_t>(g_.lpitch[k]) * g_.lh[k];
+    }
+    P.dbg_map = d_resp_ + static_cast<size_t>(first) * resp_frame_elems_;
+    P.dbg_fstride = resp_frame_elems_;
+  }
   const int smem = fused::smem_layout(P).total;
-  if (std::getenv("FLKB_DEBUG_GEOM"))
+  if (plan.debug_geom)
     std::fprintf(stderr, "flkb: R=%d tiles0=%d smem=%d ctas=%d\n", R, tiles0, smem, ctas_of(P));
   if (smem > kFusedSmemMax || R + 2 * p_.radius > 64) {  // pathological radius: staged kernels
     run_staged(frames, fstride, pitch, count, stats, s, times, first);
@@ -413,7 +436,7 @@ void DeviceBatch::run(const uint8_t* frames, size_t fstride, int pitch, int coun
   const bool aligned =
       g_.levels >= 2 && R % 4 == 0 && (P.lv[0].tiles_x == 1 || P.lv[0].tile_w % 16 == 0);
   bool want = static_cast<long>(ctas0) * count >= 4L * 148 * fused::kMinBlocks;
-  if (const char* e = std::getenv("FLKB_FUSE_PYR")) want = std::atoi(e) != 0;  // tests / tuning
+  if (plan.fuse_pyramid >= 0) want = plan.fuse_pyramid != 0;  // tests / tuning
   const int fuse_pyr = aligned && want && !pyramid_ready ? std::min(2, g_.levels - 1) : 0;
 
   cudaEvent_t ev[5] = {};
@@ -436,6 +459,8 @@ void DeviceBatch::run(const uint8_t* frames, size_t fstride, int pitch, int coun
       if (k > 0 && k < 3) P.pyr_img[k] = const_cast<uint8_t*>(L.img);
     }
     P.keys = keys + static_cast<size_t>(c0) * g_.cells;
+    if (dump_scores_)
+      P.dbg_map = d_resp_ + static_cast<size_t>(first + c0) * resp_frame_elems_;
     P.stats = stats ? st + 2 * static_cast<size_t>(c0) : nullptr;
   };
   // detection of levels [kb, ke) of n frames in one launch
@@ -476,7 +501,7 @@ void DeviceBatch::run(const uint8_t* frames, size_t fstride, int pitch, int coun
     const size_t nchunks = (static_cast<size_t>(count) * b12 + (32u << 20) - 1) / (32u << 20);
     chunk = static_cast<int>((count + nchunks - 1) / std::max<size_t>(nchunks, 1));
   }
-  if (const char* e = std::getenv("FLKB_PYR_CHUNK")) chunk = std::max(1, std::atoi(e));
+  if (plan.pyramid_chunk > 0) chunk = plan.pyramid_chunk;
   if (fuse_pyr) {
     if (times) check_cuda(cudaEventRecord(ev[1], s), "cudaEventRecord");
     if (times) check_cuda(cudaEventRecord(ev[2], s), "cudaEventRecord");
@@ -521,8 +546,7 @@ void DeviceBatch::run(const uint8_t* frames, size_t fstride, int pitch, int coun
     launched += pyr_launches;
     if (times) check_cuda(cudaEventRecord(ev[1], s), "cudaEventRecord");
     if (times) check_cuda(cudaEventRecord(ev[2], s), "cudaEventRecord");
-    static const bool pdl = !(std::getenv("FLKB_PDL") && std::atoi(std::getenv("FLKB_PDL")) == 0);
-    P.pdl_wait = pdl && pyr_launches > 0 && !times;
+    P.pdl_wait = plan.pdl && pyr_launches > 0 && !times;
     detect(0, g_.levels, 0, count, s);
     P.pdl_wait = 0;
   }

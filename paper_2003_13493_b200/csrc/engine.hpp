@@ -27,6 +27,21 @@ namespace flkb {
 constexpr int kMaxLevels = 16;
 constexpr int kCoordBits = 18;  // x0, y0 < 2^18 inside a packed cell key
 
+// Overrides of the automatic launch plan (tests, tuning tools). Set
+// explicitly through flkb_detector_set_plan / flkb_batch_set_plan; the
+// engine never reads the environment. Zero / -1 = automatic.
+struct LaunchPlan {
+  int band_rows = 0;      // rows per CTA band (0: halo-cost shape search)
+  int tiles = 0;          // level-0 column tiles (0: shape search)
+  int fuse_pyramid = -1;  // 1: two-launch plan (levels 1-2 from the level-0 CTAs), 0: one-launch plan
+  int pyramid_chunk = 0;  // frames per chunk of the two-launch plan (0: levels 1-2 <= L2 / 4)
+  int pdl = 1;            // programmatic dependent launch in the one-launch plan
+  int list_cap = 0;       // corner-list entries per CTA (0: the spare shared memory)
+  int debug_geom = 0;     // print the chosen shape to stderr
+  // key = value setter; false for an unknown key
+  bool set(const std::string& key, int value);
+};
+
 struct DetectParams {
   int epsilon = 10;
   int arc_length = 10;
@@ -35,6 +50,7 @@ struct DetectParams {
   int radius = 1;
   int cell_w = 32;
   int cell_h = 32;
+  LaunchPlan plan;
   static DetectParams from(const Config& c);
 };
 
@@ -103,6 +119,15 @@ class DeviceBatch {
                               cudaStream_t s, int first = 0, int count = 1,
                               flk_conformance* per_frame = nullptr);
 
+  // Diagnostic: run() also writes the fused kernel's u16 scores of every
+  // level into the score-map buffer download_responses() reads.
+  void set_dump_scores(bool on) { dump_scores_ = on; }
+  // Replaces the launch-plan overrides (the shape search reruns).
+  void set_plan(const LaunchPlan& plan) {
+    p_.plan = plan;
+    fused_tiles0_ = 0;
+    fused_R_ = 32;
+  }
   const Geometry& geometry() const { return g_; }
   const DetectParams& params() const { return p_; }
   // Enqueues levels [k0, levels) of the pyramid from level k0-1 (level 0 =
@@ -143,6 +168,7 @@ class DeviceBatch {
   // ccx, cmy, ccy), exact for every in-image coordinate when cell_ok_
   uint32_t cmap_[kMaxLevels][4] = {};
   bool cell_ok_ = false;
+  bool dump_scores_ = false;
   int last_launches_ = 0;
   cudaStream_t side_ = nullptr;      // chunked two-launch plan: level 1-2 launches
   std::vector<cudaEvent_t> evs_;     // its fork / per-chunk / join events        // kernels enqueued by the last run()

@@ -84,6 +84,8 @@ struct Level {
   // likewise cy (one IMAD.HI each; the host checks every in-image coordinate;
   // ccx, ccy are 0 or 1)
   uint32_t cmx, ccx, cmy, ccy;
+  size_t dbg_off;  // diagnostic score dump: level offset (u16 elements) and pitch
+  int dbg_pitch;
 };
 
 struct Params {
@@ -109,6 +111,10 @@ struct Params {
   uint32_t emask[8];  // ~0 where bit b of eps is set
   unsigned long long* keys;
   unsigned long long* stats;
+  // diagnostic: when set, every CTA writes the u16 scores of its own rows and
+  // columns (the reference's response values, 0 off corners and in the border)
+  uint16_t* dbg_map;
+  size_t dbg_fstride;
 };
 
 struct Smem {
@@ -713,6 +719,14 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_detect(const __grid_co
     }
   }
   __syncthreads();
+  if (P.dbg_map) {  // diagnostic score dump (flkb_detector_fused_responses)
+    uint16_t* out = P.dbg_map + f * P.dbg_fstride + L.dbg_off;
+    const int tw = x_hi - x_lo;
+    for (int i = tid; i < (y1 - y0) * tw; i += kThreads) {
+      const int y = y0 + i / tw, x = x_lo + i % tw;
+      out[static_cast<size_t>(y) * L.dbg_pitch + x] = tile_s[(y - fy0) * RP + (x - x_lo) + 2 * n];
+    }
+  }
 
   // --- 5. suppression + per-cell keys for the candidates in rows [y0, y1):
   //        a contiguous range of the list, since tasks are row-major

@@ -8,8 +8,10 @@
 // serially (the Hessian entries over the patch, the right-hand side of each
 // Gauss-Newton step) is accumulated serially here too, one thread per sum, in
 // pixel order. The per-pixel work (bilinear samples, residuals, products) is
-// spread over the CTA's threads. hypot is CUDA's (<= 2 ulp); it only feeds the
-// divergence / convergence comparisons.
+// spread over the CTA's threads. std::hypot is glibc's (not correctly rounded:
+// ~0.2 % of random pairs differ from the exact rounding), so the device uses
+// the same algorithm, glibc_hypot below, rather than CUDA's hypot; it feeds the
+// divergence / convergence comparisons (lk.cpp:267, 319).
 #include <algorithm>
 #include <chrono>
 #include <cmath>
@@ -17,6 +19,8 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
+
+#include <math_constants.h>
 
 #include "session.hpp"
 
@@ -40,6 +44,47 @@ __device__ __forceinline__ float sample_bilinear(const uint8_t* __restrict__ img
   const double bot = (1.0 - fx) * r1[x0] + fx * r1[x1];
   return static_cast<float>((1.0 - fy) * top + fy * bot);
 }
+
+// glibc 2.35+ __hypot (sysdeps/ieee754/dbl-64/e_hypot.c, the non-FMA kernel an
+// x86-64 build without -mfma runs: Borges' correction of sqrt(ax^2 + ay^2)),
+// operation for operation, so std::hypot's result is reproduced bit for bit.
+__device__ __forceinline__ double glibc_hypot_kernel(double ax, double ay) {
+  double h = sqrt(ax * ax + ay * ay);
+  double t1, t2;
+  if (h <= 2.0 * ay) {
+    const double delta = h - ay;
+    t1 = ax * (2.0 * delta - ax);
+    t2 = (delta - 2.0 * (ax - ay)) * delta;
+  } else {
+    const double delta = h - ax;
+    t1 = 2.0 * delta * (ax - 2.0 * ay);
+    t2 = (4.0 * delta - ay) * ay + delta * delta;
+  }
+  h -= (t1 + t2) / (2.0 * h);
+  return h;
+}
+
+}  // namespace
+
+__device__ double glibc_hypot(double x, double y) {
+  if (!isfinite(x) || !isfinite(y)) return (isinf(x) || isinf(y)) ? CUDART_INF : x + y;
+  x = fabs(x);
+  y = fabs(y);
+  const double ax = x < y ? y : x, ay = x < y ? x : y;
+  const double kScale = 0x1p-600, kLarge = 0x1p+511, kTiny = 0x1p-511, kEps = 0x1p-54;
+  if (ax > kLarge) {
+    if (ay <= ax * kEps) return ax + ay;
+    return glibc_hypot_kernel(ax * kScale, ay * kScale) / kScale;
+  }
+  if (ay < kTiny) {
+    if (ax >= ay / kEps) return ax + ay;
+    return glibc_hypot_kernel(ax / kScale, ay / kScale) * kScale;
+  }
+  if (ay <= ax * kEps) return ax + ay;
+  return glibc_hypot_kernel(ax, ay);
+}
+
+namespace {
 
 // det_small (lk.cpp:74-102)
 __device__ double det_small(const double* in, int n) {
@@ -226,7 +271,7 @@ __global__ void __launch_bounds__(256) k_track(Levels lv, const int* __restrict_
     double ty = ty0 / scale;
     const int patch = T.patch, half = patch / 2, npx = patch * patch, dims = T.dims;
     const double ax = T.ax, ay = T.ay;
-    const double max_step = 0.5 * hypot(static_cast<double>(w), static_cast<double>(h));
+    const double max_step = 0.5 * glibc_hypot(static_cast<double>(w), static_cast<double>(h));
     const size_t base = (static_cast<size_t>(slot) * L + k) * kMaxPx;
     // the level's inverse Hessian in shared memory (read by every thread for
     // the identical update each iteration)
@@ -275,7 +320,7 @@ __global__ void __launch_bounds__(256) k_track(Levels lv, const int* __restrict_
       int d = 2;
       if (has_gain(tp.mode)) gain += delta[d++];
       if (has_offset(tp.mode)) offset += delta[d++];
-      const double step = hypot(delta[0], delta[1]);
+      const double step = glibc_hypot(delta[0], delta[1]);
       if (step > max_step || !(gain > -1.0) || !isfinite(step)) {
         status = 1;  // DIVERGED
         aborted = true;
@@ -301,7 +346,26 @@ __global__ void __launch_bounds__(256) k_track(Levels lv, const int* __restrict_
   }
 }
 
+__global__ void k_hypot(const double* x, const double* y, double* out, int n) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = glibc_hypot(x[i], y[i]);
+}
+
 }  // namespace
+
+void debug_hypot(const double* x, const double* y, double* out, int n) {
+  if (n <= 0) return;
+  const size_t bytes = sizeof(double) * static_cast<size_t>(n);
+  double* d = nullptr;
+  check_cuda(cudaMalloc(&d, 3 * bytes), "hypot buffers");
+  cudaMemcpy(d, x, bytes, cudaMemcpyHostToDevice);
+  cudaMemcpy(d + n, y, bytes, cudaMemcpyHostToDevice);
+  k_hypot<<<(n + 255) / 256, 256>>>(d, d + n, d + 2 * n, n);
+  count_launches(1);
+  const cudaError_t e = cudaMemcpy(out, d + 2 * n, bytes, cudaMemcpyDeviceToHost);
+  cudaFree(d);
+  check_cuda(e, "hypot kernel");
+}
 }  // namespace lk
 
 namespace {
@@ -483,8 +547,6 @@ void Session::submit(const HostImage& img, bool timed) {
   // H2D frame, H2D track records, then the graph: pyramid -> k_track (results
   // written to the mapped records).
   // Stage times are CUDA-event device times.
-  static const bool trace = std::getenv("FLKB_SESSION_TRACE") != nullptr;
-  const auto tt0 = Clock::now();
   // one contiguous DMA of the frame at the device pitch, straight from the
   // image's page-locked pixels when the rows already have that pitch, else
   // re-pitched through the pinned staging buffer (a pitched 2-D copy of a
@@ -499,7 +561,6 @@ void Session::submit(const HostImage& img, bool timed) {
   if (timed) check_cuda(cudaEventRecord(ev_[0], stream_), "event");
   check_cuda(cudaMemcpyAsync(d_frame_, src, static_cast<size_t>(pitch_) * img.height,
                              cudaMemcpyHostToDevice, stream_), "H2D frame");
-  const auto tt1 = Clock::now();
   const int n = static_cast<int>(tracks_.size());
   *reinterpret_cast<int*>(h_io_) = n;
   lk::TrackIO* io = reinterpret_cast<lk::TrackIO*>(h_io_ + kIoHeader);
@@ -514,7 +575,6 @@ void Session::submit(const HostImage& img, bool timed) {
   check_cuda(cudaGraphLaunch(graph_exec_[timed ? 1 : 0], stream_), "frame graph");
   count_launches(graph_launches_);
   submitted_ = true;
-  t_submit_ = std::chrono::duration<double, std::micro>(tt1 - tt0).count();
 }
 
 // Second half: wait for the frame graph, then the lifecycle of
@@ -523,7 +583,6 @@ void Session::complete(const HostImage& img, std::vector<flk_track_info>* out,
                        flk_frame_stats* stats, flk_conformance* conformance) {
   if (!submitted_) throw InvalidArgument("no submitted frame to complete");
   submitted_ = false;
-  static const bool trace = std::getenv("FLKB_SESSION_TRACE") != nullptr;
   DeviceGuard guard(device_);
   const int cw = cfg_.cell_width(), ch = cfg_.cell_height();
   const Geometry& g = batch_->geometry();
@@ -539,10 +598,7 @@ void Session::complete(const HostImage& img, std::vector<flk_track_info>* out,
     lv.w[k] = g.lw[k];
     lv.h[k] = g.lh[k];
   }
-  const auto tt2 = Clock::now();
   check_cuda(cudaStreamSynchronize(stream_), "pyramid + track");
-  if (trace)
-    std::fprintf(stderr, "flkb session: staging %.1f us, wait %.1f us\n", t_submit_, us_since(tt2));
   if (stats) {
     float ms_pyr = 0, ms_trk = 0;
     check_cuda(cudaEventElapsedTime(&ms_pyr, ev_[0], ev_[1]), "stage time");

@@ -46,6 +46,10 @@ struct TrackerParams {
   double convergence_epsilon, min_determinant_factor;
 };
 
+// std::hypot as glibc computes it, on the device (test hook: n pairs,
+// host arrays in and out, synchronous).
+void debug_hypot(const double* x, const double* y, double* out, int n);
+
 }  // namespace lk
 
 class Session {
@@ -87,7 +91,6 @@ class Session {
   cudaGraphExec_t graph_exec_[2] = {nullptr, nullptr};  // plain, with stage events
   int graph_launches_ = 0;
   bool submitted_ = false;
-  double t_submit_ = 0;
   uint8_t* d_frame_ = nullptr;
   uint8_t* h_frame_ = nullptr;  // pinned staging
   int pitch_ = 0;

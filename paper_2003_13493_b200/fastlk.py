@@ -103,7 +103,9 @@ EXT_SYMBOLS = [
     "flkb_batch_device_counts", "flkb_batch_device_features", "flkb_batch_device_stats",
     "flkb_batch_device_pyramid", "flkb_synth_frames_device", "flkb_kernel_launch_count",
     "flkb_batch_kernels_per_run", "flkb_detector_responses", "flkb_batch_run_device_timed",
-    "flkb_sessions_process", "flkb_features_copy", "flkb_tracks_copy", "flkb_batch_conformance"]
+    "flkb_sessions_process", "flkb_features_copy", "flkb_tracks_copy", "flkb_batch_conformance",
+    "flkb_detector_run_batch_multi", "flkb_detector_set_plan", "flkb_batch_set_plan",
+    "flkb_debug_hypot", "flkb_batch_detect_host", "flkb_detector_fused_responses"]
 
 _lib = None
 _vp = ctypes.c_void_p
@@ -168,6 +170,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
                                               ctypes.POINTER(ctypes.c_int),
                                               ctypes.POINTER(ctypes.c_size_t)]
     lib.flkb_detector_responses.argtypes = [_vp, _vp, _vp]
+    lib.flkb_detector_fused_responses.argtypes = [_vp, _vp, _vp]
     lib.flkb_batch_run_device_timed.argtypes = [_vp, _vp, ctypes.c_size_t, ctypes.c_int,
                                                 ctypes.c_int, _vp, _vp]
     lib.flk_session_create.argtypes = [_vp, ctypes.POINTER(_vp)]
@@ -180,6 +183,12 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.flkb_tracks_copy.argtypes = [_vp, _vp, ctypes.c_int]
     lib.flkb_batch_conformance.argtypes = [_vp, _vp, ctypes.c_size_t, ctypes.c_int, ctypes.c_int,
                                            ctypes.c_int, _vp, _vp, _vp]
+    lib.flkb_detector_run_batch_multi.argtypes = [_vp, _vp, ctypes.c_int, _vp, ctypes.c_int, _vp]
+    lib.flkb_detector_set_plan.argtypes = [_vp, ctypes.c_char_p, ctypes.c_int]
+    lib.flkb_batch_set_plan.argtypes = [_vp, ctypes.c_char_p, ctypes.c_int]
+    lib.flkb_debug_hypot.argtypes = [_vp, _vp, _vp, ctypes.c_int]
+    lib.flkb_batch_detect_host.argtypes = [_vp, _vp, ctypes.c_size_t, ctypes.c_int, ctypes.c_int,
+                                           _vp, _vp, _vp]
     lib.flkb_synth_frames_device.argtypes = [_vp, ctypes.c_int, ctypes.c_uint64, ctypes.c_int,
                                              ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                              ctypes.c_size_t, _vp]
@@ -364,11 +373,19 @@ class Detector(_Handle):
     """flk_detector: pyramid + FAST + fused grid NMS on the GPU."""
     _destroy = "flk_detector_destroy"
 
-    def __init__(self, config: Config, device: int | None = None):
+    def __init__(self, config: Config, device: int | None = None, plan: dict | None = None):
         super().__init__()
         _check(_lib.flk_detector_create(config.handle, ctypes.byref(self._h)))
         if device is not None:
             _check(_lib.flkb_detector_set_device(self._h, device))
+        if plan:
+            self.set_plan(**plan)
+
+    def set_plan(self, **plan) -> "Detector":
+        """flkb_detector_set_plan: launch-plan overrides (tests / tuning)."""
+        for k, v in plan.items():
+            _check(_lib.flkb_detector_set_plan(self._h, k.encode(), int(v)))
+        return self
 
     def run(self, image, stats: bool = False, conformance: bool = False):
         """Detects one frame (flk_detector_run). Returns the features as a
@@ -393,8 +410,10 @@ class Detector(_Handle):
             extra["conformance"] = {k: getattr(cf, k) for k, _ in ConformanceT._fields_}
         return (feats, extra) if extra else feats
 
-    def responses(self, image, levels: int):
-        """flkb_detector_responses: per-level float score maps of one frame."""
+    def responses(self, image, levels: int, fused: bool = False):
+        """flkb_detector_responses: per-level float score maps of one frame
+        (staged kernels); fused=True: flkb_detector_fused_responses, the
+        production fused kernel's own scores."""
         if isinstance(image, np.ndarray):
             image = Image.from_array(image)
         dims, w, h = [], image.width, image.height
@@ -403,11 +422,30 @@ class Detector(_Handle):
             w //= 2
             h //= 2
         out = np.zeros(sum(a * b for a, b in dims), np.float32)
-        _check(_lib.flkb_detector_responses(self._h, image.handle, out.ctypes.data))
+        fn = _lib.flkb_detector_fused_responses if fused else _lib.flkb_detector_responses
+        _check(fn(self._h, image.handle, out.ctypes.data))
         res, off = [], 0
         for (hh, ww) in dims:
             res.append(out[off:off + hh * ww].reshape(hh, ww))
             off += hh * ww
+        return res
+
+    def run_batch_multi(self, images, devices):
+        """flkb_detector_run_batch_multi: contiguous frame shards over several
+        GPUs (one host thread each); list of arrays in frame order."""
+        imgs = [Image.from_array(i) if isinstance(i, np.ndarray) else i for i in images]
+        n, nd = len(imgs), len(devices)
+        arr = (_vp * max(n, 1))(*[i.handle.value for i in imgs])
+        devs = (ctypes.c_int * nd)(*devices)
+        outs = (_vp * max(n, 1))()
+        _check(_lib.flkb_detector_run_batch_multi(self._h, devs, nd, arr, n, outs))
+        res = []
+        for i in range(n):
+            h = _vp(outs[i])
+            try:
+                res.append(_features_to_array(h))
+            finally:
+                _lib.flk_features_destroy(h)
         return res
 
     def run_batch(self, images):
@@ -444,6 +482,12 @@ class DeviceBatch(_Handle):
         self.frame_capacity = _lib.flkb_batch_frame_capacity(self._h)
         self.kernels_per_run = _lib.flkb_batch_kernels_per_run(self._h)
 
+    def set_plan(self, **plan) -> "DeviceBatch":
+        """flkb_batch_set_plan: launch-plan overrides for this batch."""
+        for k, v in plan.items():
+            _check(_lib.flkb_batch_set_plan(self._h, k.encode(), int(v)))
+        return self
+
     def run_device(self, frames_ptr: int, frame_stride: int, row_pitch: int, count: int,
                    stream: int = 0, with_stats: bool = False) -> None:
         _check(_lib.flkb_batch_run_device(self._h, frames_ptr, frame_stride, row_pitch, count,
@@ -462,6 +506,13 @@ class DeviceBatch(_Handle):
                  stream: int = 0) -> None:
         _check(_lib.flkb_batch_run_host(self._h, frames_ptr, frame_stride, row_pitch, count,
                                         stream or None))
+
+    def detect_host(self, frames_ptr: int, frame_stride: int, row_pitch: int, count: int,
+                    counts_ptr: int | None, feats_ptr: int | None, stream: int = 0) -> None:
+        """flkb_batch_detect_host: host frames in, host feature lists out,
+        copies overlapped with the kernels (asynchronous on `stream`)."""
+        _check(_lib.flkb_batch_detect_host(self._h, frames_ptr, frame_stride, row_pitch, count,
+                                           counts_ptr, feats_ptr, stream or None))
 
     def download(self, first: int, count: int, counts_ptr: int | None, feats_ptr: int | None,
                  stream: int = 0) -> None:
@@ -513,6 +564,16 @@ def synth_frames_device(frames_ptr: int, kind: int, first_frame: int, count: int
     load_library()
     _check(_lib.flkb_synth_frames_device(frames_ptr, kind, first_frame, count, width, height,
                                          row_pitch, frame_stride, stream or None))
+
+
+def debug_hypot(x: np.ndarray, y: np.ndarray) -> np.ndarray:
+    """flkb_debug_hypot: the tracker's device hypot on host pairs (test hook)."""
+    load_library()
+    x = np.ascontiguousarray(x, np.float64)
+    y = np.ascontiguousarray(y, np.float64)
+    out = np.zeros_like(x)
+    _check(_lib.flkb_debug_hypot(x.ctypes.data, y.ctypes.data, out.ctypes.data, x.size))
+    return out
 
 
 def _sync_default_stream():

@@ -1,0 +1,161 @@
+"""Multi-device host batches, launch-plan overrides, session-handle checks and
+the tracker's device hypot, through the C ABI."""
+import ctypes
+import math
+
+import numpy as np
+import pytest
+
+import paper_2003_13493_b200 as fl
+from paper_2003_13493_b200 import fastlk as fk
+import synth
+
+pytestmark = pytest.mark.gpu
+
+CFG = dict(epsilon=10, N=9, score_kind="sad_b", l=3, w=1, h=8, n=1)
+
+
+def _cfg(**kw):
+    return fl.Config(**dict(CFG, **kw))
+
+
+@pytest.mark.parametrize("devices", [[0], [0, 0], [0, 0, 0], [0, 0, 0, 0, 0, 0, 0, 0]])
+def test_run_batch_multi_matches_single_device(devices):
+    """Frame shards over a device list (device 0 listed several times on a
+    one-GPU box): per-frame results bit-identical to flkb_detector_run_batch
+    and to single flk_detector_run calls, whatever the list."""
+    frames = [synth.texture(300 + f, 752, 480) for f in range(37)]
+    want = fl.Detector(_cfg()).run_batch(frames)
+    det = fl.Detector(_cfg())
+    got = det.run_batch_multi(frames, devices)
+    assert len(got) == len(want)
+    for i, (a, b) in enumerate(zip(got, want)):
+        assert len(a) == len(b) and (a == b).all(), i
+    # cached per-device pipelines are reused on the next call
+    again = det.run_batch_multi(frames[:5], devices)
+    for a, b in zip(again, want[:5]):
+        assert (a == b).all()
+    single = fl.Detector(_cfg())
+    for i in (0, 18, 36):
+        assert (single.run(frames[i]) == want[i]).all()
+
+
+def test_run_batch_multi_more_devices_than_frames():
+    frames = [synth.noise(10 + f, 320, 240) for f in range(3)]
+    cfg = dict(l=2, h=16)
+    want = fl.Detector(_cfg(**cfg)).run_batch(frames)
+    got = fl.Detector(_cfg(**cfg)).run_batch_multi(frames, [0] * 5)
+    for a, b in zip(got, want):
+        assert (a == b).all()
+    assert fl.Detector(_cfg(**cfg)).run_batch_multi([], [0, 0]) == []
+
+
+def test_run_batch_multi_errors():
+    lib = fl.load_library()
+    det = fl.Detector(_cfg())
+    frames = [fl.Image.from_array(synth.texture(f, 752, 480)) for f in range(4)]
+    arr = (ctypes.c_void_p * 4)(*[i.handle.value for i in frames])
+    outs = (ctypes.c_void_p * 4)(*([12345] * 4))
+    bad = (ctypes.c_int * 2)(0, 999)
+    assert lib.flkb_detector_run_batch_multi(det.handle, bad, 2, arr, 4, outs) == fk.FLK_E_INVALID_ARG
+    none = (ctypes.c_int * 1)(0)
+    assert lib.flkb_detector_run_batch_multi(det.handle, none, 0, arr, 4, outs) == fk.FLK_E_INVALID_ARG
+    assert lib.flkb_detector_run_batch_multi(det.handle, None, 1, arr, 4, outs) == fk.FLK_E_INVALID_ARG
+    # a frame of another size: dimension mismatch, every out NULL
+    det.run(synth.texture(0, 752, 480))
+    odd = fl.Image.from_array(synth.texture(9, 320, 240))
+    arr2 = (ctypes.c_void_p * 2)(frames[0].handle.value, odd.handle.value)
+    outs2 = (ctypes.c_void_p * 2)(1, 1)
+    dev = (ctypes.c_int * 2)(0, 0)
+    assert lib.flkb_detector_run_batch_multi(det.handle, dev, 2, arr2, 2, outs2) == fk.FLK_E_DIMENSION
+    assert outs2[0] is None and outs2[1] is None
+
+
+def test_set_device_drops_cached_pipelines():
+    """flkb_detector_set_device resets the single-frame runner AND
+    the host-batch pipelines, so later batches run on the selected GPU."""
+    frames = [synth.texture(40 + f, 752, 480) for f in range(6)]
+    det = fl.Detector(_cfg())
+    a = det.run_batch(frames)
+    lib = fl.load_library()
+    assert lib.flkb_detector_set_device(det.handle, fl.device_count()) == fk.FLK_E_INVALID_ARG
+    last = fl.device_count() - 1
+    assert lib.flkb_detector_set_device(det.handle, last) == 0
+    b = det.run_batch(frames)
+    for x, y in zip(a, b):
+        assert (x == y).all()
+
+
+def test_launch_plan_api():
+    det = fl.Detector(_cfg())
+    with pytest.raises(fl.ConfigError):
+        det.set_plan(no_such_key=1)
+    img = synth.noise(5, 752, 480)
+    base = det.run(img)
+    for plan in ({"fuse_pyramid": 0}, {"fuse_pyramid": 1}, {"band_rows": 16, "tiles": 3},
+                 {"pdl": 0}, {"list_cap": 300}):
+        assert (fl.Detector(_cfg(), plan=plan).run(img) == base).all(), plan
+    batch = fl.DeviceBatch(det, 752, 480, 2)
+    with pytest.raises(fl.ConfigError):
+        batch.set_plan(bogus=3)
+
+
+def test_duplicate_sessions_rejected():
+    """the same session twice in one flkb_sessions_process call is
+    an invalid argument (it would stage two frames into one session)."""
+    cfg = fl.Config(**dict(CFG, l=2, h=16, target_count=20))
+    s = fl.Session(cfg)
+    img = synth.texture(3, 256, 192)
+    with pytest.raises(fl.InvalidArgument):
+        fl.sessions_process([s, s], [img, img])
+    # the session is still usable
+    s.process(img)
+
+
+def test_stats_batch_failure_leaves_no_handles():
+    """a failing frame in the stats path of
+    flkb_detector_run_batch leaves every out NULL, as the pipelined path."""
+    lib = fl.load_library()
+    det = fl.Detector(_cfg(l=2, h=16))
+    good = fl.Image.from_array(synth.texture(1, 256, 192))
+    other = fl.Image.from_array(synth.texture(2, 256, 192))
+    arr = (ctypes.c_void_p * 2)(good.handle.value, other.handle.value)
+    outs = (ctypes.c_void_p * 2)()
+    stats = (fk.FrameStats * 2)()
+    assert lib.flkb_detector_run_batch(det.handle, arr, 2, outs, stats) == 0
+    for i in range(2):
+        lib.flk_features_destroy(ctypes.c_void_p(outs[i]))
+    # a second frame of another size fails the size latch: error, no out survives
+    small = fl.Image.from_array(synth.texture(3, 128, 96))
+    arr = (ctypes.c_void_p * 2)(good.handle.value, small.handle.value)
+    outs = (ctypes.c_void_p * 2)()
+    assert lib.flkb_detector_run_batch(det.handle, arr, 2, outs, stats) == fk.FLK_E_DIMENSION
+    assert outs[0] is None and outs[1] is None
+
+
+def test_device_hypot_matches_glibc():
+    """The tracker's step length (lk.cpp:319) and max step (lk.cpp:267) use
+    std::hypot: the device reproduces glibc's algorithm bit for bit, including
+    the ~0.2 % of pairs where glibc is not correctly rounded."""
+    libm = ctypes.CDLL("libm.so.6")
+    libm.hypot.restype = ctypes.c_double
+    libm.hypot.argtypes = [ctypes.c_double, ctypes.c_double]
+    rng = np.random.default_rng(7)
+    n = 200_000
+    scale = rng.choice([1e-3, 1e-1, 1.0, 10.0, 1e3, 1e-200, 1e200, 1e-310], n)
+    x = rng.uniform(-1, 1, n) * scale
+    y = rng.uniform(-1, 1, n) * scale * rng.choice([1.0, 1e-3, 1e-8, 1e-20], n)
+    edge = np.array([0.0, -0.0, 3.0, math.inf, -math.inf, math.nan, 1e308, 5e-324, 752.0, 480.0])
+    x = np.concatenate([x, edge, edge[::-1]])
+    y = np.concatenate([y, edge[::-1], edge])
+    got = fl.debug_hypot(x, y)
+    want = np.array([libm.hypot(a, b) for a, b in zip(x.tolist(), y.tolist())])
+    same = (got == want) | (np.isnan(got) & np.isnan(want))
+    assert same.all(), f"{(~same).sum()} pairs differ, e.g. {x[~same][:3]}, {y[~same][:3]}"
+    # the convergence test compares against the threshold: a step exactly at
+    # the reference's convergence_epsilon decides identically
+    eps = 0.01
+    pts = np.array([[0.006, 0.008], [0.0070710678118654755, 0.0070710678118654755]])
+    g = fl.debug_hypot(pts[:, 0], pts[:, 1])
+    w = np.array([libm.hypot(a, b) for a, b in pts.tolist()])
+    assert ((g <= eps) == (w <= eps)).all() and (g == w).all()

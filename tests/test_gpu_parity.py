@@ -35,13 +35,12 @@ def make_config(cfg):
 
 @pytest.mark.parametrize("fuse", ["0", "1"])
 @pytest.mark.parametrize("case", GOLDEN, ids=[c[0] for c in GOLDEN])
-def test_golden_cases_through_c_abi(golden, case, fuse, monkeypatch):
-    monkeypatch.setenv("FLKB_FUSE_PYR", fuse)
+def test_golden_cases_through_c_abi(golden, case, fuse):
     meta, arrays = golden
     name, fam, f, w, h, cfg, full = case
     m = meta[name]
     img = synth.frame(fam, f, w, h)
-    det = fl.Detector(make_config(cfg))
+    det = fl.Detector(make_config(cfg), plan={"fuse_pyramid": int(fuse)})
     feats, extra = det.run(img, stats=True)
     assert len(feats) == m["count"]
     assert hashlib.sha256(feats.tobytes()).hexdigest() == m["sha256"]
@@ -57,8 +56,8 @@ def test_golden_cases_through_c_abi(golden, case, fuse, monkeypatch):
 
 
 @pytest.mark.parametrize("seed", range(48))
-def test_random_configs_vs_oracle(orc, seed, monkeypatch):
-    monkeypatch.setenv("FLKB_FUSE_PYR", str(seed % 2))
+def test_random_configs_vs_oracle(orc, seed):
+    plan = {"fuse_pyramid": seed % 2}
     rng = np.random.default_rng(500 + seed)
     l = int(rng.integers(1, 5))
     w = int(rng.integers(8 << (l - 1), 400))
@@ -69,11 +68,11 @@ def test_random_configs_vs_oracle(orc, seed, monkeypatch):
                score_kind=["sad_b", "sad_a", "mt"][seed % 3], l=l, w=int(rng.integers(1, 3)),
                h=int(rng.integers(1, 9)), n=int(rng.integers(1, 5)))
     p = oracle.make_params(**cfg)
-    det = fl.Detector(make_config(cfg))
+    det = fl.Detector(make_config(cfg), plan=plan)
     resp = det.responses(img, l)
     for k, (a, b) in enumerate(zip(resp, orc.responses(img, p))):
         assert (a == b).all(), f"level {k} score map differs"
-    det2 = fl.Detector(make_config(cfg))
+    det2 = fl.Detector(make_config(cfg), plan=plan)
     feats, extra = det2.run(img, stats=True)
     ref, st = orc.detect(img, p)
     assert (feats == ref).all()
@@ -123,21 +122,53 @@ def read_device(ptr: int, nbytes: int) -> np.ndarray:
     return torch.as_tensor(_DevBuf(ptr, nbytes), device="cuda").cpu().numpy()
 
 
+@pytest.mark.parametrize("seed", range(24))
+def test_fused_kernel_score_maps_vs_oracle(orc, seed):
+    """The production fused kernel's own scores (each CTA's shared-memory score
+    tile, dumped for its rows and columns) equal the reference response maps
+    (fast.cpp:273-303) on every pixel of every level, for random configs,
+    both pyramid plans and forced band/tile shapes."""
+    rng = np.random.default_rng(900 + seed)
+    l = int(rng.integers(1, 5))
+    w = int(rng.integers(8 << (l - 1), 800))
+    h = int(rng.integers(8 << (l - 1), 500))
+    fam = ["noise", "texture", "quant4", "blocks"][seed % 4]
+    img = synth.frame(fam, seed, w, h)
+    cfg = dict(epsilon=int(rng.choice([0, 1, 5, 10, 25, 80, 255])), N=int(rng.integers(9, 17)),
+               score_kind=["sad_b", "sad_a", "mt"][seed % 3], l=l, w=int(rng.integers(1, 3)),
+               h=int(rng.integers(1, 9)), n=int(rng.integers(1, 4)))
+    plan = {"fuse_pyramid": seed % 2}
+    if seed % 3 == 2:
+        plan.update(band_rows=int(rng.choice([8, 12, 20, 32])), tiles=int(rng.integers(1, 6)))
+    got = fl.Detector(make_config(cfg), plan=plan).responses(img, l, fused=True)
+    for k, (a, b) in enumerate(zip(got, orc.responses(img, oracle.make_params(**cfg)))):
+        assert (a == b).all(), f"level {k}: {(a != b).sum()} pixels differ"
+
+
+def test_fused_kernel_score_maps_c4(orc):
+    """The bench configuration (752x480, l=3, FAST-9 SAD-B): fused scores of
+    every level against the oracle, noise and texture."""
+    cfg = dict(epsilon=10, N=9, score_kind="sad_b", l=3, w=1, h=8, n=1)
+    for img in (synth.texture(0, 752, 480), synth.noise(1, 752, 480)):
+        got = fl.Detector(make_config(cfg)).responses(img, 3, fused=True)
+        for a, b in zip(got, orc.responses(img, oracle.make_params(**cfg))):
+            assert (a == b).all()
+
+
 @pytest.mark.parametrize("fuse", ["0", "1"])
 @pytest.mark.parametrize("shape", ["", "20:1", "16:2", "12:3", "8:5"])
-def test_pyramid_levels_match_oracle(orc, fuse, shape, monkeypatch):
-    """Levels >= 1 from the standalone downsampling kernel (FLKB_FUSE_PYR=0)
+def test_pyramid_levels_match_oracle(orc, fuse, shape):
+    """Levels >= 1 from the standalone downsampling kernel (fuse_pyramid=0)
     and from the level-0 CTAs of the fused kernel (=1: levels 1-2 written from
     the staged rows, the rest downsampled), over several band/tile shapes."""
     import torch
-    monkeypatch.setenv("FLKB_FUSE_PYR", fuse)
+    plan = {"fuse_pyramid": int(fuse)}
     if shape:
         r, t = shape.split(":")
-        monkeypatch.setenv("FLKB_BAND_ROWS", r)
-        monkeypatch.setenv("FLKB_TILES", t)
+        plan.update(band_rows=int(r), tiles=int(t))
     W, H, L = 753, 481, 4
     frames = np.stack([synth.texture(i, W, H) for i in range(3)])
-    det = fl.Detector(fl.Config(l=L, h=4))
+    det = fl.Detector(fl.Config(l=L, h=4), plan=plan)
     batch = fl.DeviceBatch(det, W, H, 3)
     d = torch.from_numpy(frames).cuda()
     batch.run_device(d.data_ptr(), W * H, W, 3)
@@ -206,14 +237,13 @@ def test_conformance_tally_matches_reference_semantics(orc):
 
 
 @pytest.mark.parametrize("fuse", ["0", "1"])
-def test_batch_conformance_tally_per_frame(orc, fuse, monkeypatch):
+def test_batch_conformance_tally_per_frame(orc, fuse):
     """flkb_batch_conformance: the GPU tally of every frame
     of a device batch equals the reference conformance_check of that frame."""
     import torch
-    monkeypatch.setenv("FLKB_FUSE_PYR", fuse)
     W, H, n = 320, 240, 12
     cfg = dict(epsilon=10, N=9, score_kind="mt", l=3, w=1, h=4, n=2)
-    det = fl.Detector(make_config(cfg))
+    det = fl.Detector(make_config(cfg), plan={"fuse_pyramid": int(fuse)})
     batch = fl.DeviceBatch(det, W, H, n)
     pitch = 320
     d = torch.zeros((n, H, pitch), dtype=torch.uint8, device="cuda")
@@ -277,15 +307,13 @@ def test_unaligned_pitch_uses_plain_loads_and_matches(orc):
 
 @pytest.mark.parametrize("cap", [0, 256, 1000])
 @pytest.mark.parametrize("kind", ["sad_b", "sad_a"])
-def test_dense_corners_multi_round_list(orc, kind, cap, monkeypatch):
+def test_dense_corners_multi_round_list(orc, kind, cap):
     """eps = 0 on noise makes ~40 % of pixels corners; with the corner list
-    capped (FLKB_LIST_CAP) every band overflows it and the kernel scores and
+    capped (plan list_cap) every band overflows it and the kernel scores and
     suppresses in several rounds. Results must not depend on the cap."""
-    if cap:
-        monkeypatch.setenv("FLKB_LIST_CAP", str(cap))
     img = synth.noise(77, 752, 480)
     cfg = dict(epsilon=0, N=9, score_kind=kind, l=2, w=1, h=16, n=1)
-    feats, extra = fl.Detector(make_config(cfg)).run(img, stats=True)
+    feats, extra = fl.Detector(make_config(cfg), plan={"list_cap": cap}).run(img, stats=True)
     ref, st = orc.detect(img, oracle.make_params(**cfg))
     assert (feats == ref).all()
     assert extra["stats"]["nms_candidates"] == st.candidates
@@ -315,17 +343,15 @@ def test_large_radius(orc, n):
 
 @pytest.mark.parametrize("fuse", ["0", "1"])
 @pytest.mark.parametrize("shape", ["60:1", "32:3", "12:5", "8:8", "20:2", "18:2", "16:7"])
-def test_forced_band_shapes(orc, shape, fuse, monkeypatch):
+def test_forced_band_shapes(orc, shape, fuse):
     """Results must not depend on the band rows / column tiles the engine picks,
     nor on whether pyramid levels 1-2 come from the fused kernel."""
     r, t = shape.split(":")
-    monkeypatch.setenv("FLKB_BAND_ROWS", r)
-    monkeypatch.setenv("FLKB_TILES", t)
-    monkeypatch.setenv("FLKB_FUSE_PYR", fuse)
+    plan = {"band_rows": int(r), "tiles": int(t), "fuse_pyramid": int(fuse)}
     img = synth.noise(31, 752, 480)
     for cfg in (dict(epsilon=10, N=9, score_kind="sad_b", l=3, w=1, h=8, n=1),
                 dict(epsilon=20, N=12, score_kind="sad_a", l=2, w=2, h=2, n=2)):
-        feats, extra = fl.Detector(make_config(cfg)).run(img, stats=True)
+        feats, extra = fl.Detector(make_config(cfg), plan=plan).run(img, stats=True)
         ref, st = orc.detect(img, oracle.make_params(**cfg))
         assert (feats == ref).all()
         assert extra["stats"]["nms_comparisons"] == st.comparisons
@@ -353,85 +379,109 @@ def test_batch_api_with_stats_matches_single_runs():
         assert stats[i].nms_comparisons == single[i][1]["stats"]["nms_comparisons"]
 
 
-def _full_batch_check(orc, cfg, W, H, n, sample, cell=None, kind=1):
-    """A BASELINE-sized device batch: exact parity on a sample of frames, and
-    size-independent properties on every frame (one feature per cell, cells in
-    row-major order, positive scores, levels in range, features inside the
-    frame and inside their cell)."""
+_REF_CACHE = {}
+
+
+def _full_batch_check(ref, cfg, W, H, n, cell=None, kind=1, plan=None):
+    """A BASELINE-sized device batch, EVERY frame bit-exact against the
+    reference build run frame-parallel on the same frames (refh_detect =
+    detect_frame + the capi flatten, capi.cpp:232-274), plus the structural
+    properties (one feature per cell, row-major cells, features inside their
+    cell)."""
     import torch
     c = make_config(cfg)
     if cell:
         c.set_cell_size_px(*cell)
-    det = fl.Detector(c)
+    det = fl.Detector(c, plan=plan)
     batch = fl.DeviceBatch(det, W, H, n)
     pitch = (W + 15) // 16 * 16
     d = torch.empty((n, H, pitch), dtype=torch.uint8, device="cuda")
     fl.synth_frames_device(d.data_ptr(), kind, 3000, n, W, H, pitch, pitch * H)
     batch.run_device(d.data_ptr(), pitch * H, pitch, n)
     torch.cuda.synchronize()
-    res = batch.results(n)
+    cap = batch.frame_capacity
+    counts = np.zeros(n, np.int32)
+    feats = np.zeros(n * cap, fl.FEATURE_DTYPE)
+    batch.download(0, n, counts.ctypes.data, feats.ctypes.data, 0)
+    torch.cuda.synchronize()
+    feats = feats.reshape(n, cap)
     p = oracle.make_params(**cfg, cell_width_px=cell[0] if cell else 0,
                            cell_height_px=cell[1] if cell else 0)
     cw, ch = p.cell_width(), p.cell_height()
     cols, rows = (W + cw - 1) // cw, (H + ch - 1) // ch
-    for f in res:
-        assert len(f) <= cols * rows
-        key = f["cell_y"].astype(np.int64) * cols + f["cell_x"]
-        assert (np.diff(key) > 0).all()
+    assert cap == cols * rows
+    key = (kind, W, H, n, tuple(sorted(cfg.items())), cell)
+    if key not in _REF_CACHE:
+        # the device generator is bit-identical to the host one
+        # (test_device_synth_matches_host_generator); download, don't re-synthesise
+        frames = d[:, :, :W].contiguous().cpu().numpy()
+        _REF_CACHE.clear()
+        _REF_CACHE[key] = ref.detect_batch(frames, p)
+    rc, rf = _REF_CACHE[key]
+    bad = [i for i in range(n) if counts[i] != rc[i] or (feats[i, :counts[i]] != rf[i, :rc[i]]).any()]
+    assert not bad, f"{len(bad)} of {n} frames differ from the reference, first {bad[:8]}"
+    for i in range(n):
+        f = feats[i, :counts[i]]
+        k = f["cell_y"].astype(np.int64) * cols + f["cell_x"]
+        assert (np.diff(k) > 0).all()
         assert (f["score"] > 0).all() and (f["level"] >= 0).all() and (f["level"] < cfg["l"]).all()
         assert (f["x"] // cw == f["cell_x"]).all() and (f["y"] // ch == f["cell_y"]).all()
-        assert (f["x"] < W).all() and (f["y"] < H).all()
-    rng = np.random.default_rng(n)
-    fam = {0: synth.noise, 1: synth.texture}[kind]
-    for i in sorted(set(rng.integers(0, n, sample).tolist()) | {0, n - 1}):
-        ref, _ = orc.detect(fam(3000 + i, W, H), p)
-        assert (res[i] == ref).all(), f"frame {i}"
-    return res
+    return counts, feats
 
 
-@pytest.mark.parametrize("fuse", ["0", "1"])
-def test_c4_full_batch_4096(orc, fuse, monkeypatch):
+@pytest.mark.parametrize("fuse", [0, 1])
+def test_c4_full_batch_4096(ref, fuse):
     """BASELINE configs[3]: 4096 frames of 752x480, l=3 in one device batch
-    (the bench workload), both pyramid plans."""
-    monkeypatch.setenv("FLKB_FUSE_PYR", fuse)
+    (the bench workload), both pyramid plans, every frame against the reference."""
     cfg = dict(epsilon=10, N=9, score_kind="sad_b", l=3, w=1, h=8, n=1)
-    res = _full_batch_check(orc, cfg, 752, 480, 4096, 12)
-    assert sum(len(f) for f in res) > 4096 * 300
+    counts, _ = _full_batch_check(ref, cfg, 752, 480, 4096, plan={"fuse_pyramid": fuse})
+    assert counts.sum() > 4096 * 300
 
 
-def test_chunked_two_launch_plan_is_invariant(monkeypatch):
+def test_chunked_two_launch_plan_is_invariant():
     """The two-launch plan's chunking (level 1-2 launches on a side stream
     overlapping the next chunk's level-0 launch) never changes a result: every
     chunk size gives the unchunked feature lists."""
     import torch
     W, H, n = 752, 480, 1200
     cfg = dict(epsilon=10, N=9, score_kind="sad_b", l=3, w=1, h=8, n=1)
-    det = fl.Detector(make_config(cfg))
+    det = fl.Detector(make_config(cfg), plan={"fuse_pyramid": 1})
     pitch = 768
     d = torch.empty((n, H, pitch), dtype=torch.uint8, device="cuda")
     fl.synth_frames_device(d.data_ptr(), 1, 77, n, W, H, pitch, pitch * H)
-    monkeypatch.setenv("FLKB_FUSE_PYR", "1")
     out = {}
-    for chunk in ("1200", "1", "7", "256", "599"):
-        monkeypatch.setenv("FLKB_PYR_CHUNK", chunk)
-        batch = fl.DeviceBatch(det, W, H, n)
+    for chunk in (1200, 1, 7, 256, 599):
+        batch = fl.DeviceBatch(det, W, H, n).set_plan(pyramid_chunk=chunk)
         batch.run_device(d.data_ptr(), pitch * H, pitch, n)
         torch.cuda.synchronize()
         out[chunk] = np.concatenate(batch.results(n))
     for chunk, f in out.items():
-        assert len(f) == len(out["1200"]) and (f == out["1200"]).all(), chunk
+        assert len(f) == len(out[1200]) and (f == out[1200]).all(), chunk
 
 
-def test_c3_full_batch_256_16px_cells(orc):
-    """BASELINE configs[2]: 256 frames of 1920x1080, l=4, FAST-12, 16x16 cells."""
+def test_c3_full_batch_256_16px_cells(ref):
+    """BASELINE configs[2]: 256 frames of 1920x1080, l=4, FAST-12, 16x16 cells,
+    every frame against the reference composition at 16x16 cells."""
     cfg = dict(epsilon=10, N=12, score_kind="sad_b", l=4, w=1, h=2, n=1)
-    _full_batch_check(orc, cfg, 1920, 1080, 256, 4, cell=(16, 16))
+    _full_batch_check(ref, cfg, 1920, 1080, 256, cell=(16, 16))
 
 
-def test_c5_full_batch_4k(orc):
-    """BASELINE configs[4]: 3840x2160, l=5, FAST-10 (per-GPU batch of 32)."""
+def test_c3_twin_full_batch_256(ref):
+    """C3's twin the reference API expresses (32x16 cells: w=1, h=2)."""
+    cfg = dict(epsilon=10, N=12, score_kind="sad_b", l=4, w=1, h=2, n=1)
+    _full_batch_check(ref, cfg, 1920, 1080, 256)
+
+
+def test_c5_full_batch_4k(ref):
+    """BASELINE configs[4]: 3840x2160, l=5, FAST-10, 64 frames, every frame."""
     cfg = dict(epsilon=10, N=10, score_kind="sad_b", l=5, w=1, h=2, n=1)
-    _full_batch_check(orc, cfg, 3840, 2160, 32, 2)
+    _full_batch_check(ref, cfg, 3840, 2160, 64)
+
+
+def test_c1_full_batch_mt(ref):
+    """BASELINE configs[0] as a batch: 752x480, l=1, FAST-9 MT, 512 frames."""
+    cfg = dict(epsilon=10, N=9, score_kind="mt", l=1, w=1, h=32, n=1)
+    _full_batch_check(ref, cfg, 752, 480, 512)
 
 
 @pytest.mark.parametrize("l,w,h,cell,size", [

@@ -73,3 +73,53 @@ def test_gloo_world2_gather(total):
         n, f = fake_frame(g, cap)
         assert counts[g] == n
         assert (feats[g] == f).all()
+
+
+def _detect_worker(rank, world, port, total, q):
+    """One rank of the N>1 path with the reference build standing in for the
+    GPU (no device here): detect this rank's contiguous shard, then gather."""
+    import sys
+    import torch.distributed as dist
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, root)
+    import oracle
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    start, n = shard_range(total, rank, world)
+    orc, ref = oracle.load_oracle(), oracle.load_reference()
+    p = oracle.make_params(epsilon=10, N=9, score_kind="sad_b", l=3, w=1, h=2, n=1)
+    frames = np.stack([orc.synth(1, start + i, 256, 192) for i in range(n)])
+    counts, feats = ref.detect_batch(frames, p, workers=1)
+    res = gather_features(counts, feats, total)
+    if rank == 0:
+        q.put((res[0].tolist(), res[1].tobytes()))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("total", [5, 12])
+def test_gloo_world2_detect_and_gather(total):
+    """World size 2 over gloo: each rank detects its shard of S2 frames
+    (global frame indices) and rank 0 gathers; the result equals one
+    process detecting every frame (bench.py's N>1 parity path)."""
+    import oracle
+    if oracle.load_reference() is None:
+        pytest.skip("reference build unavailable")
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_detect_worker, args=(r, 2, port, total, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    counts, raw = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    orc, ref = oracle.load_oracle(), oracle.load_reference()
+    p = oracle.make_params(epsilon=10, N=9, score_kind="sad_b", l=3, w=1, h=2, n=1)
+    frames = np.stack([orc.synth(1, i, 256, 192) for i in range(total)])
+    want_c, want_f = ref.detect_batch(frames, p)
+    assert counts == want_c.tolist()
+    got = np.frombuffer(raw, np.int32).reshape(total, -1)
+    assert (got == np.ascontiguousarray(want_f).view(np.int32).reshape(total, -1)).all()
+    assert sum(counts) > 0

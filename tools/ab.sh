@@ -1,10 +1,11 @@
 #!/bin/bash
-# A/B timing of env variants: tools/ab.sh "FLKB_FUSE_PYR=0" "FLKB_FUSE_PYR=1" ...
+# A/B timing of launch-plan variants: tools/ab.sh "fuse_pyramid=0" "fuse_pyramid=1" ...
+# (each argument is passed as bench.py --plan; "" = the automatic plan)
 # Each variant's bench line -> gpurun_out/ab_<i>.json; a summary on stdout.
 mkdir -p gpurun_out
 i=0
 for v in "$@"; do
-  env $v timeout 300 python bench.py --no-cpu-baseline --no-extras --e2e-steps 2 ${BENCH_ARGS} \
+  timeout 300 python bench.py --plan "$v" --no-cpu-baseline --no-parity --no-extras --e2e-steps 2 ${BENCH_ARGS} \
     > gpurun_out/ab_$i.json 2> gpurun_out/ab_$i.err
   python - "$v" gpurun_out/ab_$i.json <<'PY'
 import json, sys

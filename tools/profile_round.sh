@@ -8,10 +8,10 @@
 #     session sequence
 mkdir -p gpurun_out
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
-  --log-file gpurun_out/launches.csv python bench.py --batch 4096 --steps 2 --warmup 3 \
+  --log-file gpurun_out/launches.csv python bench.py --global-batch 4096 --no-parity --steps 2 --warmup 3 \
   --e2e-steps 1 --no-cpu-baseline --no-extras > gpurun_out/ncu_launch.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_detect -s 6 -c 2 \
-  -o gpurun_out/prof_full -f python bench.py --batch 4096 --steps 1 --warmup 3 --e2e-steps 1 \
+  -o gpurun_out/prof_full -f python bench.py --global-batch 4096 --no-parity --steps 1 --warmup 3 --e2e-steps 1 \
   --no-cpu-baseline --no-extras > gpurun_out/ncu_full.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_track|k_template" \
   -s 20 -c 4 -o gpurun_out/prof_lk -f python -c "

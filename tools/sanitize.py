@@ -31,8 +31,7 @@ def main():
         (synth.noise(4, 160, 96), dict(epsilon=0, N=9, score_kind="sad_b", l=1, w=1, h=32, n=1), "0"),
     ]
     for img, cfg, fuse in cases:
-        os.environ["FLKB_FUSE_PYR"] = fuse
-        det = fl.Detector(fl.Config(**cfg))
+        det = fl.Detector(fl.Config(**cfg), plan={"fuse_pyramid": int(fuse)})
         feats, extra = det.run(img, stats=True, conformance=True)
         ref, st = orc.detect(img, oracle.make_params(**cfg))
         assert (feats == ref).all() and extra["stats"]["nms_comparisons"] == st.comparisons
@@ -40,20 +39,17 @@ def main():
         maps = det.responses(img, cfg["l"])
         for a, b in zip(maps, orc.responses(img, oracle.make_params(**cfg))):
             assert (a == b).all()
-    os.environ["FLKB_LIST_CAP"] = "256"  # multi-round corner lists
-    img = synth.noise(5, 200, 120)
+    img = synth.noise(5, 200, 120)  # multi-round corner lists
     cfg = dict(epsilon=0, N=9, score_kind="sad_b", l=2, w=1, h=16, n=1)
-    feats = fl.Detector(fl.Config(**cfg)).run(img)
+    feats = fl.Detector(fl.Config(**cfg), plan={"list_cap": 256}).run(img)
     assert (feats == orc.detect(img, oracle.make_params(**cfg))[0]).all()
-    del os.environ["FLKB_LIST_CAP"]
     # a device batch in the chunked two-launch plan (side-stream level 1-2
     # launches) and its GPU conformance tally
     import torch
-    os.environ["FLKB_FUSE_PYR"] = "1"
-    os.environ["FLKB_PYR_CHUNK"] = "3"
     W, H, n = 256, 160, 8
     cfg = dict(epsilon=10, N=9, score_kind="sad_b", l=3, w=1, h=8, n=1)
-    batch = fl.DeviceBatch(fl.Detector(fl.Config(**cfg)), W, H, n)
+    batch = fl.DeviceBatch(fl.Detector(fl.Config(**cfg), plan={"fuse_pyramid": 1,
+                                                               "pyramid_chunk": 3}), W, H, n)
     d = torch.empty((n, H, W), dtype=torch.uint8, device="cuda")
     fl.synth_frames_device(d.data_ptr(), 1, 40, n, W, H, W, W * H)
     batch.run_device(d.data_ptr(), W * H, W, n)
@@ -63,7 +59,6 @@ def main():
         assert (res[f] == orc.detect(synth.texture(40 + f, W, H), oracle.make_params(**cfg))[0]).all()
     total, _ = batch.conformance(d.data_ptr(), W * H, W, 0, n)
     assert total["false_positives"] == 0 and total["matched"] == sum(len(r) for r in res)
-    del os.environ["FLKB_PYR_CHUNK"]
     frames = sessions.drifting_sequence(3, 192, 128)
     scfg = dict(epsilon=10, N=9, score_kind="sad_b", l=2, w=1, h=16, n=1, target_count=12,
                 redetect_ratio=0.5, param_mode="full", max_iterations=30, convergence_epsilon=0.01)

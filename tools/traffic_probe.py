@@ -16,7 +16,8 @@ def main():
     import bench
     import paper_2003_13493_b200 as fl
     B, W, H, P = 4096, bench.W, bench.H, bench.PITCH
-    det = fl.Detector(fl.Config(**bench.CFG))
+    chunk = int(os.environ.get("PYR_CHUNK", "0"))  # tool option, passed as a launch plan
+    det = fl.Detector(fl.Config(**bench.CFG), plan={"pyramid_chunk": chunk} if chunk else None)
     batch = fl.DeviceBatch(det, W, H, B)
     frames = torch.empty((B, H, P), dtype=torch.uint8, device="cuda")
     st = torch.cuda.current_stream().cuda_stream
