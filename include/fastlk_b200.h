@@ -57,7 +57,10 @@ FLK_API flk_status flkb_detector_run_batch_multi(flk_detector* detector, const i
  * environment variables): keys "band_rows", "tiles" (0 = shape search),
  * "fuse_pyramid" (-1 auto, 0 one-launch plan, 1 two-launch plan),
  * "pyramid_chunk" (frames, 0 = auto), "pdl" (0/1), "list_cap" (corner-list
- * entries, 0 = auto), "debug_geom" (0/1). Results never depend on the plan.
+ * entries, 0 = auto), "debug_geom" (0/1), "staged" (1: the staged v1 kernels, one
+ * launch per stage and level with u16 score maps in HBM -- the design
+ * baseline the fused kernel is measured against). Results never depend on
+ * the plan.
  * Setting a detector's plan drops its cached device workspaces; batches take
  * the detector's plan at creation. Unknown key: FLK_E_CONFIG. */
 FLK_API flk_status flkb_detector_set_plan(flk_detector* detector, const char* key, int value);

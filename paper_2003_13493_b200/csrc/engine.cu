@@ -1,5 +1,8 @@
 // Host orchestration of the sm_100a detector kernels: geometry, device
 // buffers, launch plan, stage timing, conformance and synthetic frames.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include <atomic>
 #include <cstddef>
 #include <cstdio>
@@ -81,6 +84,8 @@ bool LaunchPlan::set(const std::string& key, int value) {
   else if (key == "pdl") pdl = value != 0;
   else if (key == "list_cap") list_cap = value <= 0 ? 0 : std::max(256, value);
   else if (key == "debug_geom") debug_geom = value != 0;
+  else if (key == "staged") staged = value != 0;
+  else if (key == "tensor_tma") tensor_tma = value != 0;
   else return false;
   return true;
 }
@@ -205,6 +210,38 @@ DeviceBatch::~DeviceBatch() {
 int DeviceBatch::kernels_per_run() const { return last_launches_ ? last_launches_ : g_.levels + 1; }
 
 namespace {
+
+// cuTensorMapEncodeTiled from the driver through the runtime's entry-point
+// query (the library links no libcuda)
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess) {
+      cudaGetLastError();
+      p = nullptr;
+    }
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }();
+  return fn;
+}
+
+// The fused kernel's staging map of one level: u8 (x, y, frame) over
+// `frames` frames, box = (stage pitch, stage rows, 1). False if the shape
+// does not fit a TMA box or the encoder is unavailable (row copies then).
+bool encode_stage_map(fused::Level& L, int frames, int box_w, int box_h) {
+  auto enc = tensor_map_encoder();
+  if (!enc || !L.tma || box_w > 256 || box_h > 256 || box_w % 16) return false;
+  const cuuint64_t dims[3] = {static_cast<cuuint64_t>(L.w), static_cast<cuuint64_t>(L.h),
+                              static_cast<cuuint64_t>(frames)};
+  const cuuint64_t strides[2] = {static_cast<cuuint64_t>(L.pitch), static_cast<cuuint64_t>(L.fstride)};
+  const cuuint32_t box[3] = {static_cast<cuuint32_t>(box_w), static_cast<cuuint32_t>(box_h), 1};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  return enc(&L.tmap, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<uint8_t*>(L.img), dims, strides,
+             box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
 
 // kMinBlocks CTAs per SM (1 KB of each CTA's share is reserved by the driver)
 constexpr int kFusedSmemTarget = (228 * 1024) / fused::kMinBlocks - 1024;
@@ -397,10 +434,12 @@ void DeviceBatch::run(const uint8_t* frames, size_t fstride, int pitch, int coun
     P.dbg_map = d_resp_ + static_cast<size_t>(first) * resp_frame_elems_;
     P.dbg_fstride = resp_frame_elems_;
   }
+  fused::finalize(P);
   const int smem = fused::smem_layout(P).total;
   if (plan.debug_geom)
     std::fprintf(stderr, "flkb: R=%d tiles0=%d smem=%d ctas=%d\n", R, tiles0, smem, ctas_of(P));
-  if (smem > kFusedSmemMax || R + 2 * p_.radius > 64) {  // pathological radius: staged kernels
+  // pathological radius (or the staged plan asked for): the staged kernels
+  if (smem > kFusedSmemMax || R + 2 * p_.radius > 64 || plan.staged) {
     run_staged(frames, fstride, pitch, count, stats, s, times, first);
     if (out_counts)
       check_cuda(cudaMemcpyAsync(out_counts, d_counts_ + first, sizeof(int) * count,
@@ -447,7 +486,7 @@ void DeviceBatch::run(const uint8_t* frames, size_t fstride, int pitch, int coun
   if (stats) check_cuda(cudaMemsetAsync(st, 0, sizeof(uint64_t) * 2 * count, s), "memset stats");
   int launched = 0;
   // frame pointers of the frames [c0, c0 + n) of this call
-  auto bind = [&](int c0) {
+  auto bind = [&](int c0, int nf) {
     for (int k = 0; k < g_.levels; ++k) {
       fused::Level& L = P.lv[k];
       L.img = k == 0 ? frames + static_cast<size_t>(c0) * fstride
@@ -457,6 +496,7 @@ void DeviceBatch::run(const uint8_t* frames, size_t fstride, int pitch, int coun
       L.tma = (reinterpret_cast<uintptr_t>(L.img) % 16 == 0) && L.pitch % 16 == 0 &&
               L.fstride % 16 == 0;
       if (k > 0 && k < 3) P.pyr_img[k] = const_cast<uint8_t*>(L.img);
+      L.tmap_ok = plan.tensor_tma && encode_stage_map(L, nf, P.sw, P.R + 2 * p_.radius + 6);
     }
     P.keys = keys + static_cast<size_t>(c0) * g_.cells;
     if (dump_scores_)
@@ -524,7 +564,7 @@ void DeviceBatch::run(const uint8_t* frames, size_t fstride, int pitch, int coun
     int ei = 1;
     for (int c0 = 0; c0 < count; c0 += chunk) {
       const int n = std::min(chunk, count - c0);
-      bind(c0);
+      bind(c0, n);
       detect(0, 1, fuse_pyr, n, s);
       launched += enqueue_pyramid(frames + static_cast<size_t>(c0) * fstride, fstride, pitch, n, s,
                                   first + c0, fuse_pyr + 1);
@@ -540,7 +580,7 @@ void DeviceBatch::run(const uint8_t* frames, size_t fstride, int pitch, int coun
       check_cuda(cudaStreamWaitEvent(s, evs_[ei], 0), "join wait");
     }
   } else {
-    bind(0);
+    bind(0, count);
     int pyr_launches = 0;
     if (!pyramid_ready) pyr_launches = enqueue_pyramid(frames, fstride, pitch, count, s, first);
     launched += pyr_launches;

@@ -38,6 +38,8 @@ struct LaunchPlan {
   int pdl = 1;            // programmatic dependent launch in the one-launch plan
   int list_cap = 0;       // corner-list entries per CTA (0: the spare shared memory)
   int debug_geom = 0;     // print the chosen shape to stderr
+  int staged = 0;         // 1: the staged v1 kernels (one launch per stage and level, u16 maps in HBM)
+  int tensor_tma = 1;     // stage each CTA's rows with one tensor-map TMA copy (0: one bulk copy per row)
   // key = value setter; false for an unknown key
   bool set(const std::string& key, int value);
 };

@@ -29,6 +29,8 @@
 //           cell_candidate_wins order (nms.cpp:41-46).
 #pragma once
 
+#include <cuda.h>
+
 #include <cstdint>
 #include <type_traits>
 
@@ -46,7 +48,10 @@ constexpr int kWarps = kThreads / 32;
 #ifndef FLKB_MIN_BLOCKS
 #define FLKB_MIN_BLOCKS 6
 #endif
-constexpr int kMinBlocks = FLKB_MIN_BLOCKS;  // CTAs per SM the register budget targets
+constexpr int kMinBlocks = FLKB_MIN_BLOCKS;
+#ifndef FLKB_KEYS
+#define FLKB_KEYS 0
+#endif  // CTAs per SM the register budget targets
 constexpr int kMaxLv = 16;
 // Stage pitch (bytes) and score-tile pitch (u16) of the radius-1 instance:
 // column tiles up to 192 px (8 plane words) fit them.
@@ -71,6 +76,11 @@ struct FastDiv {
 };
 
 struct Level {
+  // 3-D tiled TMA map of the level (x, y, frame) whose box is one CTA's
+  // stage (stage pitch x stage rows): the whole staging is one
+  // cp.async.bulk.tensor, rows and columns outside the image zero-filled
+  alignas(64) CUtensorMap tmap;
+  int tmap_ok;
   const uint8_t* img;  // frame 0, row 0
   size_t fstride;
   int pitch, w, h;
@@ -115,6 +125,9 @@ struct Params {
   // columns (the reference's response values, 0 off corners and in the border)
   uint16_t* dbg_map;
   size_t dbg_fstride;
+  // shared-memory layout and corner-list capacity, filled by the host
+  // (finalize()) so the kernel does not recompute them
+  int sm_stage, sm_planes, sm_cm, sm_list, sm_scan, sm_skeys, sm_bar, cap;
 };
 
 struct Smem {
@@ -158,6 +171,19 @@ __host__ __device__ inline Smem smem_layout(const Params& p) {
   off += 16;
   s.total = off;
   return s;
+}
+
+// Host: stores the layout and list capacity in the parameters the kernel reads.
+inline void finalize(Params& p) {
+  const Smem s = smem_layout(p);
+  p.sm_stage = s.stage;
+  p.sm_planes = s.planes;
+  p.sm_cm = s.cm;
+  p.sm_list = s.list;
+  p.sm_scan = s.scan;
+  p.sm_skeys = s.skeys;
+  p.sm_bar = s.bar;
+  p.cap = list_capacity(p);
 }
 
 // ------------------------------------------------------------ primitives
@@ -328,7 +354,6 @@ struct TaskIter {
 template <int N, int KIND, int RADIUS>
 __global__ void __launch_bounds__(kThreads, kMinBlocks) k_detect(const __grid_constant__ Params P) {
   extern __shared__ __align__(128) uint8_t smem[];
-  const Smem S = smem_layout(P);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 
   // stage / score-tile pitches: compile-time in the radius-1 instance (the host
@@ -354,17 +379,17 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_detect(const __grid_co
   const int cx_lo = max(x_lo - n, 3), cx_hi = min(x_hi + n, w - 3);  // FAST columns
   const int cy_lo = max(fy0, 3), cy_hi = min(y1 + n, h - 3);         // FAST rows
 
-  uint8_t* stage = smem + S.stage;
-  uint32_t* planes = reinterpret_cast<uint32_t*>(smem + S.planes);
-  uint16_t* tile_s = reinterpret_cast<uint16_t*>(smem + S.planes);
-  uint32_t* cm = reinterpret_cast<uint32_t*>(smem + S.cm);
-  uint16_t* list = reinterpret_cast<uint16_t*>(smem + S.list);
-  int* scan = reinterpret_cast<int*>(smem + S.scan);
+  uint8_t* stage = smem + P.sm_stage;
+  uint32_t* planes = reinterpret_cast<uint32_t*>(smem + P.sm_planes);
+  uint16_t* tile_s = reinterpret_cast<uint16_t*>(smem + P.sm_planes);
+  uint32_t* cm = reinterpret_cast<uint32_t*>(smem + P.sm_cm);
+  uint16_t* list = reinterpret_cast<uint16_t*>(smem + P.sm_list);
+  int* scan = reinterpret_cast<int*>(smem + P.sm_scan);
   // planes: low half (bit planes 0-3) and high half (4-7) in separate arrays
   // so a warp's 16-byte accesses to consecutive words are bank-conflict free
   const int half = (P.R + 2 * n + 6) * P.nw_max * 4;
-  uint32_t* skeys = reinterpret_cast<uint32_t*>(smem + S.skeys);
-  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + S.bar);
+  uint32_t* skeys = reinterpret_cast<uint32_t*>(smem + P.sm_skeys);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + P.sm_bar);
 
   // cell rows touched by the suppressed rows [y0, y1) of level k
   const int cr0 = P.div_ch(y0 << k);
@@ -379,7 +404,25 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_detect(const __grid_co
   const int sx0 = gx0 - bx0;  // multiple of 16
   int row_bytes = min(bx0 + SW, L.pitch) - gx0;
   row_bytes = min(row_bytes, ((w + 15) & ~15) - gx0);
-  if (L.tma) {
+  if (L.tmap_ok) {
+    // the stage's rows [iy0, iy0 + rows) x columns [bx0, bx0 + SW) of frame f
+    // in one tensor copy (negative or past-the-edge coordinates read zeros)
+    if (tid == 0) {
+      const uint32_t b = static_cast<uint32_t>(__cvta_generic_to_shared(bar));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(b));
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      const uint32_t bytes = static_cast<uint32_t>(SW * (P.R + 2 * n + 6));
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(bytes)
+                   : "memory");
+      const uint32_t dst = static_cast<uint32_t>(__cvta_generic_to_shared(stage));
+      asm volatile(
+          "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+          " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(dst),
+          "l"(reinterpret_cast<uint64_t>(&L.tmap)), "r"(bx0), "r"(iy0), "r"(f), "r"(b)
+          : "memory");
+    }
+  } else if (L.tma) {
     row_bytes &= ~15;
     if (tid == 0) {
       const uint32_t b = static_cast<uint32_t>(__cvta_generic_to_shared(bar));
@@ -399,11 +442,11 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_detect(const __grid_co
   if (local_keys)
     for (int i = tid; i < slots; i += kThreads) skeys[i] = 0u;
   __syncthreads();
-  if (L.tma) {
-    // one row copy per thread (the barrier is armed), then every thread waits
-    // for the transaction count
+  if (L.tma || L.tmap_ok) {
+    // row copies (one per thread, the barrier is armed) unless the tensor
+    // copy is in flight, then one warp waits for the transaction count
     const uint32_t b = static_cast<uint32_t>(__cvta_generic_to_shared(bar));
-    for (int y = ya + tid; y < yb; y += kThreads) {
+    for (int y = ya + tid; !L.tmap_ok && y < yb; y += kThreads) {
       const uint32_t dst = static_cast<uint32_t>(
           __cvta_generic_to_shared(stage + (y - iy0) * SW + sx0));
       const uint8_t* src = frame + static_cast<size_t>(y) * L.pitch + gx0;
@@ -412,14 +455,20 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_detect(const __grid_co
               "r"(dst), "l"(src), "r"(row_bytes), "r"(b)
           : "memory");
     }
-    uint32_t done = 0;
-    while (!done) {  // suspend hint: sleep in the barrier unit rather than re-issue
-      asm volatile(
-          "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0, %2; selp.u32 %0, 1, 0, p; }"
-          : "=r"(done)
-          : "r"(b), "r"(20000)
-          : "memory");
+    // one warp polls the transaction count (each poll is an issued
+    // instruction sequence); the others wait at the CTA barrier, which
+    // also orders the copied rows before their reads
+    if (warp == 0) {
+      uint32_t done = 0;
+      while (!done) {  // suspend hint: sleep in the barrier unit rather than re-issue
+        asm volatile(
+            "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0, %2; selp.u32 %0, 1, 0, p; }"
+            : "=r"(done)
+            : "r"(b), "r"(20000)
+            : "memory");
+      }
     }
+    __syncthreads();
   }
 
   // --- 1b. level-0 CTAs write pyramid levels 1 (and 2) of their own rows
@@ -610,7 +659,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_detect(const __grid_co
   // (read after the scoring barrier)
   if (pre0 >= 0) scan[kWarps + 1] = base + pre0;
   if (pre1 >= 0) scan[kWarps + 2] = base + pre1;
-  const int cap = list_capacity(P);
+  const int cap = P.cap;
   const int row_tb = L.div_nw(tb), j_tb = tb - row_tb * nw;
   // Writes the entries with list index in [w0, w0 + cap) to list[index - w0].
   auto build = [&](int w0) {
@@ -820,6 +869,52 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_detect(const __grid_co
           }
         }
       };
+#if FLKB_KEYS
+      // A/B variant: the warp combines its
+      // survivors' 32-bit keys before the shared atomics -- FLKB_KEYS=1 groups
+      // lanes by cell (match.any + redux.max, one ATOMS.MAX per distinct cell
+      // of the warp), FLKB_KEYS=2 is the paper's shfl_xor butterfly over
+      // packed keys when every survivor of the warp falls in one cell
+      // (per-lane atomics otherwise). Radius 1, shared keys, no counters.
+      if (!P.stats && RADIUS == 1 && local_keys) {
+        for (int eb = w0 + warp * 32; eb < m_end; eb += kThreads) {  // warp-uniform trips
+          const int e = eb + lane;
+          uint32_t key = 0;
+          int slot = -1;
+          if (e < m_end) {
+            const int ent = list[e - off];
+            const int y = cy_lo + (ent >> 10), xs = ent & 1023;
+            const int x = bx0 + xs;
+            const uint16_t* row = tile_s + (y - fy0) * rp + xs + tcol;
+            const int sc = row[0];
+            const int e0 = max(max(row[-rp - 1], row[-rp]), max(row[-rp + 1], row[-1]));
+            const int l0 = max(max(row[1], row[rp - 1]), max(row[rp], row[rp + 1]));
+            if (x >= nx_lo && x < nx_hi && sc != 0 && e0 < sc && l0 <= sc) {
+              key = mad_fma(static_cast<uint32_t>(sc), P.pow2[20],
+                            kc - mad_fma(static_cast<uint32_t>(y), P.pow2[10], static_cast<uint32_t>(x)));
+              slot = static_cast<int>(mad_fma(__umulhi(static_cast<uint32_t>(y), cmy),
+                                              static_cast<uint32_t>(P.cols),
+                                              __umulhi(static_cast<uint32_t>(x), cmx)));
+            }
+          }
+#if FLKB_KEYS == 1
+          const unsigned grp = __match_any_sync(0xffffffffu, slot);
+          const uint32_t kmax = __reduce_max_sync(grp, key);
+          if (slot >= 0 && lane == __ffs(grp) - 1) atomicMax(kbase + slot, kmax);
+#else
+          const int s0 = __shfl_sync(0xffffffffu, slot, __ffs(__ballot_sync(0xffffffffu, slot >= 0)) - 1);
+          if (__all_sync(0xffffffffu, slot < 0 || slot == s0)) {
+            uint32_t k = key;
+#pragma unroll
+            for (int o = 16; o; o >>= 1) k = max(k, __shfl_xor_sync(0xffffffffu, k, o));
+            if (lane == 0 && k) atomicMax(kbase + s0, k);
+          } else if (slot >= 0) {
+            atomicMax(kbase + slot, key);
+          }
+#endif
+        }
+      } else
+#endif
       if (P.stats)
         suppress(std::true_type{});
       else
