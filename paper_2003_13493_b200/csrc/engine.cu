@@ -416,7 +416,7 @@ void DeviceBatch::run(const uint8_t* frames, size_t fstride, int pitch, int coun
   // levels otherwise score a band in several rounds)
   if (P.list_cap == 0) {
     const int spare = (kFusedSmemTarget - fused::smem_layout(P).total) / 2 & ~7;
-    if (spare > 0) P.list_cap = fused::list_capacity(P) + spare;
+    if (spare > 0) P.list_cap = fused::smem_layout(P).list_entries + spare;
   }
   for (int k = 0; k < g_.levels && cell_ok_; ++k) {
     P.lv[k].cmx = cmap_[k][0];

@@ -127,12 +127,21 @@ struct Params {
   size_t dbg_fstride;
   // shared-memory layout and corner-list capacity, filled by the host
   // (finalize()) so the kernel does not recompute them
-  int sm_stage, sm_planes, sm_cm, sm_list, sm_scan, sm_skeys, sm_bar, cap;
+  int sm_stage, sm_planes, sm_cm, sm_list, sm_scan, sm_skeys, sm_bar, sm_xrow, cap;
 };
 
 struct Smem {
-  int stage, planes, cm, list, scan, skeys, bar, total;
+  int stage, planes, cm, list, scan, skeys, bar, xrow, list_entries, total;
 };
+
+#ifndef FLKB_XROW
+#define FLKB_XROW 1
+#endif
+// Cross-row mask exchange of the mask phase (phase 3): 4 uint4 arrays of
+// ring_rows x nw words, ring_rows = kThreads / nw + 3; bounded over nw <= nw_max.
+__host__ __device__ inline int xrow_bytes(int nw_max) {
+  return FLKB_XROW ? 64 * (kThreads + 3 * nw_max) : 0;
+}
 
 // Corner-list capacity (u16 entries); a band with more corners is scored in
 // several rounds.
@@ -153,13 +162,19 @@ __host__ __device__ inline Smem smem_layout(const Params& p) {
   s.planes = off;  // [2 halves][img_rows][nw_max][4 planes]; the score tile aliases it later
   const int pl = img_rows * p.nw_max * 32;
   const int rt = fast_rows * p.rp * 2;
+  // the mask phase's cross-row exchange follows the planes; it is dead once
+  // the masks exist, so it overlaps the tile's tail and the corner list
+  s.xrow = (off + pl + 15) & ~15;
+  const int xrow_end = s.xrow + xrow_bytes(p.nw_max);
   off += pl > rt ? pl : rt;
-  off = (off + 127) & ~127;
-  s.cm = off;
-  off += fast_rows * p.nw_max * 4;
   off = (off + 15) & ~15;
   s.list = off;
-  off += list_capacity(p) * 2;
+  s.list_entries = list_capacity(p);
+  if (s.list + 2 * s.list_entries < xrow_end) s.list_entries = ((xrow_end - s.list) / 2 + 7) & ~7;
+  off += s.list_entries * 2;
+  off = (off + 15) & ~15;
+  s.cm = off;
+  off += fast_rows * p.nw_max * 4;
   off = (off + 15) & ~15;
   s.scan = off;
   off += (kWarps + 4) * 4;
@@ -183,7 +198,8 @@ inline void finalize(Params& p) {
   p.sm_scan = s.scan;
   p.sm_skeys = s.skeys;
   p.sm_bar = s.bar;
-  p.cap = list_capacity(p);
+  p.sm_xrow = s.xrow;
+  p.cap = s.list_entries;
 }
 
 // ------------------------------------------------------------ primitives
@@ -544,6 +560,128 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_detect(const __grid_co
 
   // --- 3. bit-sliced corner masks for the FAST rows
   const int fast_rows = cy_hi - cy_lo;
+#if FLKB_XROW
+  // Antipodal ring positions i, i + 8 (o_{i+8} = -o_i) give
+  //   dark_i(p) = bright_{i+8}(p + o_i),  bright_i(p) = dark_{i+8}(p + o_i)
+  // under the saturating thresholds sat(c -+ eps) (I(q) + eps < I(p) either
+  // way), so only the 7 positions pointing down (dy > 0) and position 4 are
+  // compared; the 7 pointing up are the down masks of the rows 1-3 above,
+  // shifted by dx lanes, and position 12 is position 4 of the same row
+  // shifted by 3 (fast.cpp:221-247 decides exactly the same). The CTA walks
+  // its rows in waves of kThreads / nw rows (one (row, word) per thread):
+  // pass A compares and publishes the down masks in a ring of wave + 3 rows,
+  // pass B derives the up masks from the three rows above and runs the
+  // segment tests. Rows cy_lo-3 .. cy_lo-1 only feed the rows below them.
+  {
+    const uint32_t (&E)[8] = P.emask;  // eps bit masks, constant-bank operands
+    const int stride = P.nw_max * 4;
+    const int wave = L.div_nw(kThreads);  // rows per wave
+    const int ring = wave + 3;
+    const int tr = L.div_nw(tid), j = tid - tr * nw;
+    const bool lane_on = tr < wave;
+    uint4* xv = reinterpret_cast<uint4*>(smem + P.sm_xrow);  // [4][ring][nw]
+    const int vs = ring * nw;
+    const int ytop = cy_lo - 3;
+    int sbase = 0;  // ring slot of row w0
+    for (int w0 = ytop; w0 < cy_hi; w0 += wave) {
+      const int y = w0 + tr;
+      const bool on = lane_on && y < cy_hi;
+      int slot = sbase + tr;
+      if (slot >= ring) slot -= ring;
+      uint32_t dk[16], bk[16];
+      if (on) {
+        // pass A: clamped thresholds sat(c - eps), sat(c + eps) of row y,
+        // then positions 4 (3,0), 5 (3,1), 11 (-3,1), 6 (2,2), 10 (-2,2),
+        // 7 (1,3), 8 (0,3), 9 (-1,3)
+        const uint32_t* pl = planes + j * 4 + (y - iy0) * stride;
+        const uint32_t* ph = pl + half;
+        auto load_planes = [&](int dy, uint32_t (&q)[8]) {
+          const uint4 u = *reinterpret_cast<const uint4*>(pl + dy * stride);
+          const uint4 v = *reinterpret_cast<const uint4*>(ph + dy * stride);
+          q[0] = u.x; q[1] = u.y; q[2] = u.z; q[3] = u.w;
+          q[4] = v.x; q[5] = v.y; q[6] = v.z; q[7] = v.w;
+        };
+        uint32_t c[8], lo[8], hi[8], br = 0, cy = 0;
+        load_planes(0, c);
+#pragma unroll
+        for (int b = 0; b < 8; ++b) {
+          // plain C so ptxas can take E[b] straight from the constant bank
+          lo[b] = c[b] ^ E[b] ^ br;
+          br = (~c[b] & E[b]) | (~c[b] & br) | (E[b] & br);
+          hi[b] = c[b] ^ E[b] ^ cy;
+          cy = (c[b] & E[b]) | (c[b] & cy) | (E[b] & cy);
+        }
+#pragma unroll
+        for (int b = 0; b < 8; ++b) {  // saturate: no ring byte is < 0 or > 255
+          lo[b] &= ~br;
+          hi[b] |= cy;
+        }
+#pragma unroll
+        for (int dy = 0; dy <= 3; ++dy) {
+          uint32_t q[8];
+          if (dy == 0) {
+#pragma unroll
+            for (int b = 0; b < 8; ++b) q[b] = c[b];
+          } else {
+            load_planes(dy, q);
+          }
+#pragma unroll
+          for (int i = 4; i <= 11; ++i) {
+            if (ring_dy(i) != dy) continue;
+            const int dx = ring_dx(i);
+            uint32_t sh[8];
+#pragma unroll
+            for (int b = 0; b < 8; ++b) sh[b] = shift_fma(q[b], dx, P.pow2);
+            dk[i] = sliced_less(sh, lo);
+            bk[i] = sliced_less(hi, sh);
+          }
+        }
+        xv[slot * nw + j] = make_uint4(dk[5], dk[11], bk[5], bk[11]);
+        xv[vs + slot * nw + j] = make_uint4(dk[6], dk[10], bk[6], bk[10]);
+        xv[2 * vs + slot * nw + j] = make_uint4(dk[7], dk[8], dk[9], bk[7]);
+        *reinterpret_cast<uint2*>(xv + 3 * vs + slot * nw + j) = make_uint2(bk[8], bk[9]);
+      }
+      __syncthreads();
+      if (on && y >= cy_lo) {
+        // pass B: the up positions from the rows above (ring slots y-1..y-3)
+        const int s1 = slot >= 1 ? slot - 1 : slot - 1 + ring;
+        const int s2 = slot >= 2 ? slot - 2 : slot - 2 + ring;
+        const int s3 = slot >= 3 ? slot - 3 : slot - 3 + ring;
+        const uint4 a = xv[s1 * nw + j];           // row y-1: dk5, dk11, bk5, bk11
+        const uint4 b2 = xv[vs + s2 * nw + j];     // row y-2: dk6, dk10, bk6, bk10
+        const uint4 c3 = xv[2 * vs + s3 * nw + j]; // row y-3: dk7, dk8, dk9, bk7
+        const uint2 d3 = *reinterpret_cast<const uint2*>(xv + 3 * vs + s3 * nw + j);  // bk8, bk9
+        dk[3] = shift_fma(a.w, 3, P.pow2);
+        bk[3] = shift_fma(a.y, 3, P.pow2);
+        dk[13] = shift_fma(a.z, -3, P.pow2);
+        bk[13] = shift_fma(a.x, -3, P.pow2);
+        dk[2] = shift_fma(b2.w, 2, P.pow2);
+        bk[2] = shift_fma(b2.y, 2, P.pow2);
+        dk[14] = shift_fma(b2.z, -2, P.pow2);
+        bk[14] = shift_fma(b2.x, -2, P.pow2);
+        dk[1] = shift_fma(d3.y, 1, P.pow2);
+        bk[1] = shift_fma(c3.z, 1, P.pow2);
+        dk[0] = d3.x;
+        bk[0] = c3.y;
+        dk[15] = shift_fma(c3.w, -1, P.pow2);
+        bk[15] = shift_fma(c3.x, -1, P.pow2);
+        dk[12] = shift_fma(bk[4], -3, P.pow2);
+        bk[12] = shift_fma(dk[4], -3, P.pow2);
+        const uint32_t corner = sliced_arc<N>(dk) | sliced_arc<N>(bk);
+        // owned bits [3, 29) that fall inside the FAST columns
+        const int xb = bx0 + kOwn * j;
+        const int lo_b = max(3, cx_lo - xb), hi_b = min(29, cx_hi - xb);
+        const uint32_t valid = hi_b > lo_b ? ((hi_b >= 32 ? 0xFFFFFFFFu : ((1u << hi_b) - 1u)) &
+                                              ~((1u << lo_b) - 1u))
+                                           : 0u;
+        cm[(y - cy_lo) * nw + j] = corner & valid;
+      }
+      sbase += wave;
+      if (sbase >= ring) sbase -= ring;
+      if (w0 + wave < cy_hi) __syncthreads();  // the next wave reuses the ring
+    }
+  }
+#else
   {
     const uint32_t (&E)[8] = P.emask;  // eps bit masks, constant-bank operands
     const int tasks = max(fast_rows, 0) * nw;
@@ -610,6 +748,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_detect(const __grid_co
       cm[t] = corner & valid;
     }
   }
+#endif
   __syncthreads();
 
   // --- 4. one CTA-wide corner list (row-major task order) from a block scan
