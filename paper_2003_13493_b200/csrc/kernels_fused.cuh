@@ -474,7 +474,10 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_detect(const __grid_co
     // one warp polls the transaction count (each poll is an issued
     // instruction sequence); the others wait at the CTA barrier, which
     // also orders the copied rows before their reads
-    if (warp == 0) {
+#ifndef FLKB_WAIT_ALL
+#define FLKB_WAIT_ALL 0
+#endif
+    if (FLKB_WAIT_ALL || warp == 0) {
       uint32_t done = 0;
       while (!done) {  // suspend hint: sleep in the barrier unit rather than re-issue
         asm volatile(
@@ -484,7 +487,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_detect(const __grid_co
             : "memory");
       }
     }
-    __syncthreads();
+    if (!FLKB_WAIT_ALL) __syncthreads();
   }
 
   // --- 1b. level-0 CTAs write pyramid levels 1 (and 2) of their own rows
@@ -583,6 +586,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_detect(const __grid_co
     const int vs = ring * nw;
     const int ytop = cy_lo - 3;
     int sbase = 0;  // ring slot of row w0
+#pragma unroll 1
     for (int w0 = ytop; w0 < cy_hi; w0 += wave) {
       const int y = w0 + tr;
       const bool on = lane_on && y < cy_hi;
@@ -678,7 +682,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_detect(const __grid_co
       }
       sbase += wave;
       if (sbase >= ring) sbase -= ring;
-      if (w0 + wave < cy_hi) __syncthreads();  // the next wave reuses the ring
+      __syncthreads();  // the next wave reuses the ring; after the last, cm is complete
     }
   }
 #else
@@ -748,8 +752,8 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_detect(const __grid_co
       cm[t] = corner & valid;
     }
   }
-#endif
   __syncthreads();
+#endif
 
   // --- 4. one CTA-wide corner list (row-major task order) from a block scan
   //        of per-task corner counts; the score tile (aliasing the dead
@@ -941,8 +945,9 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_detect(const __grid_co
       const int m_end = resident ? e_hi : min(w0 + cap, e_hi);
       // the loop is instantiated with and without the counters, so the
       // fast path carries no per-candidate stats test
-      auto suppress = [&](auto with_stats) {
+      auto suppress = [&](auto with_stats, auto local) {
         constexpr bool STATS = decltype(with_stats)::value;
+        constexpr bool LOCAL = decltype(local)::value;
         for (int e = w0 + tid; e < m_end; e += kThreads) {
           const int ent = list[e - off];
           const int y = cy_lo + (ent >> 10), xs = ent & 1023;
@@ -950,7 +955,9 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_detect(const __grid_co
           if (x < nx_lo || x >= nx_hi) continue;  // halo column of a neighbouring tile
           const uint16_t* row = tile_s + (y - fy0) * rp + xs + tcol;
           const int s = row[0];
-          if (s == 0) continue;  // a corner whose score is 0 (MT, eps 0) is no candidate
+          // a corner whose score is 0 (MT, eps 0) is no candidate; a SAD score
+          // sums >= N positive terms, so it is > 0 for every corner
+          if (KIND == kMt && s == 0) continue;
           if constexpr (STATS) {
             bool keep = true;
             ++n_cand;
@@ -990,7 +997,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_detect(const __grid_co
               }
             if (!keep) continue;
           }
-          if (local_keys) {
+          if (LOCAL) {
             // 32-bit key inside the CTA: score, then smaller y, then smaller x
             // (the level is fixed per CTA), as s << 20 | (1023 - (y - y0)) << 10
             // | (1023 - (x - x_lo)), built with IMADs; the cell with one
@@ -1054,10 +1061,14 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_detect(const __grid_co
         }
       } else
 #endif
-      if (P.stats)
-        suppress(std::true_type{});
+      if (P.stats && local_keys)
+        suppress(std::true_type{}, std::true_type{});
+      else if (P.stats)
+        suppress(std::true_type{}, std::false_type{});
+      else if (local_keys)
+        suppress(std::false_type{}, std::true_type{});
       else
-        suppress(std::false_type{});
+        suppress(std::false_type{}, std::false_type{});
       if (resident) break;
     }
   }
