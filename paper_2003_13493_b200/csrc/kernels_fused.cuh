@@ -134,13 +134,10 @@ struct Smem {
   int stage, planes, cm, list, scan, skeys, bar, xrow, list_entries, total;
 };
 
-#ifndef FLKB_XROW
-#define FLKB_XROW 1
-#endif
 // Cross-row mask exchange of the mask phase (phase 3): 4 uint4 arrays of
 // ring_rows x nw words, ring_rows = kThreads / nw + 3; bounded over nw <= nw_max.
 __host__ __device__ inline int xrow_bytes(int nw_max) {
-  return FLKB_XROW ? 64 * (kThreads + 3 * nw_max) : 0;
+  return 64 * (kThreads + 3 * nw_max);
 }
 
 // Corner-list capacity (u16 entries); a band with more corners is scored in
@@ -563,7 +560,6 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_detect(const __grid_co
 
   // --- 3. bit-sliced corner masks for the FAST rows
   const int fast_rows = cy_hi - cy_lo;
-#if FLKB_XROW
   // Antipodal ring positions i, i + 8 (o_{i+8} = -o_i) give
   //   dark_i(p) = bright_{i+8}(p + o_i),  bright_i(p) = dark_{i+8}(p + o_i)
   // under the saturating thresholds sat(c -+ eps) (I(q) + eps < I(p) either
@@ -685,75 +681,6 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_detect(const __grid_co
       __syncthreads();  // the next wave reuses the ring; after the last, cm is complete
     }
   }
-#else
-  {
-    const uint32_t (&E)[8] = P.emask;  // eps bit masks, constant-bank operands
-    const int tasks = max(fast_rows, 0) * nw;
-    TaskIter it(tid, nw, L.div_nw);
-    for (int t = tid; t < tasks; t += kThreads, it.next()) {
-      const int y = cy_lo + it.row, j = it.j;
-      const int r = y - iy0;  // stage/plane row of the centre
-      // plane rows r-3..r+3 of word j: two pointers (low / high plane halves)
-      // bumped by one row per step, no per-row multiply
-      const int stride = P.nw_max * 4;
-      const uint32_t* pl = planes + j * 4 + (r - 3) * stride;
-      const uint32_t* ph = pl + half;
-      auto load_planes = [&](const uint32_t* a, const uint32_t* b, uint32_t (&q)[8]) {
-        const uint4 u = *reinterpret_cast<const uint4*>(a);
-        const uint4 v = *reinterpret_cast<const uint4*>(b);
-        q[0] = u.x; q[1] = u.y; q[2] = u.z; q[3] = u.w;
-        q[4] = v.x; q[5] = v.y; q[6] = v.z; q[7] = v.w;
-      };
-      // c - eps and c + eps mod 256; the lanes where they wrap (borrow br:
-      // c < eps, carry cy: c + eps > 255) can have no dark resp. bright ring
-      // pixel under sat(c -+ eps), so they are cleared once from the arcs
-      // rather than by clamping 16 threshold planes
-      uint32_t c[8], lo[8], hi[8], br = 0, cy = 0;
-      load_planes(pl + 3 * stride, ph + 3 * stride, c);
-#pragma unroll
-      for (int b = 0; b < 8; ++b) {
-        // plain C so ptxas can take E[b] straight from the constant bank
-        lo[b] = c[b] ^ E[b] ^ br;
-        br = (~c[b] & E[b]) | (~c[b] & br) | (E[b] & br);
-        hi[b] = c[b] ^ E[b] ^ cy;
-        cy = (c[b] & E[b]) | (c[b] & cy) | (E[b] & cy);
-      }
-      uint32_t dk[16], bk[16];
-#pragma unroll
-      for (int dy = -3; dy <= 3; ++dy, pl += stride, ph += stride) {
-        uint32_t q[8];
-        load_planes(pl, ph, q);
-#pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          if (ring_dy(i) != dy || i == 12) continue;
-          const int dx = ring_dx(i);
-          uint32_t s[8];
-#pragma unroll
-          for (int b = 0; b < 8; ++b) s[b] = shift_fma(q[b], dx, P.pow2);
-          dk[i] = sliced_less(s, lo);
-          bk[i] = sliced_less(hi, s);
-        }
-      }
-      // ring positions 4 (3,0) and 12 (-3,0) are antipodal in one row:
-      // I(p-3) + eps < I(p) is bright_4 at p-3, I(p) + eps < I(p-3) is dark_4
-      // at p-3 (the saturations of sat(c -+ eps) drop out of both forms), so
-      // position 12 is position 4 shifted by three bit lanes -- exact on the
-      // owned bits [3, 29), since bright_4 / dark_4 hold on bits [0, 29) once
-      // their wrapped-threshold lanes are cleared
-      dk[12] = shl_fma(bk[4] & ~cy, P.pow2[3]);
-      bk[12] = shl_fma(dk[4] & ~br, P.pow2[3]);
-      uint32_t corner = (sliced_arc<N>(dk) & ~br) | (sliced_arc<N>(bk) & ~cy);
-      // owned bits [3, 29) that fall inside the FAST columns
-      const int xb = bx0 + kOwn * j;
-      const int lo_b = max(3, cx_lo - xb), hi_b = min(29, cx_hi - xb);
-      const uint32_t valid = hi_b > lo_b ? ((hi_b >= 32 ? 0xFFFFFFFFu : ((1u << hi_b) - 1u)) &
-                                            ~((1u << lo_b) - 1u))
-                                         : 0u;
-      cm[t] = corner & valid;
-    }
-  }
-  __syncthreads();
-#endif
 
   // --- 4. one CTA-wide corner list (row-major task order) from a block scan
   //        of per-task corner counts; the score tile (aliasing the dead
