@@ -175,6 +175,7 @@ DeviceBatch::DeviceBatch(const DetectParams& p, int device, int width, int heigh
   d_feats_ = dalloc<flk_feature>(static_cast<size_t>(g_.cells) * cap, "features");
   d_counts_ = dalloc<int>(cap, "counts");
   d_stats_ = dalloc<uint64_t>(2 * cap, "stats");
+  d_phase_ = dalloc<unsigned long long>(2, "phase cycles");
   check_cuda(cudaMemset(d_keys_, 0, sizeof(unsigned long long) * g_.cells * cap), "memset keys");
   // the staged score maps' pitch padding is never written: zeroed once so a
   // whole-map download reads defined bytes
@@ -200,6 +201,7 @@ DeviceBatch::~DeviceBatch() {
   cudaFree(d_feats_);
   cudaFree(d_counts_);
   cudaFree(d_stats_);
+  cudaFree(d_phase_);
   for (cudaEvent_t e : evs_) cudaEventDestroy(e);
   if (side_) cudaStreamDestroy(side_);
   cudaFree(d_naive_);
@@ -484,6 +486,13 @@ void DeviceBatch::run(const uint8_t* frames, size_t fstride, int pitch, int coun
     check_cuda(cudaEventRecord(ev[0], s), "cudaEventRecord");
   }
   if (stats) check_cuda(cudaMemsetAsync(st, 0, sizeof(uint64_t) * 2 * count, s), "memset stats");
+  // a timed stats run splits the fused launches' time into the response and
+  // the suppression phases by the kernel's own cycle counts
+  const bool split = stats && times;
+  if (split) {
+    check_cuda(cudaMemsetAsync(d_phase_, 0, 2 * sizeof(unsigned long long), s), "memset phases");
+    P.phase_cycles = d_phase_;
+  }
   int launched = 0;
   // frame pointers of the frames [c0, c0 + n) of this call
   auto bind = [&](int c0, int nf) {
@@ -604,18 +613,26 @@ void DeviceBatch::run(const uint8_t* frames, size_t fstride, int pitch, int coun
     cudaEventElapsedTime(&b, ev[1], ev[2]);
     cudaEventElapsedTime(&c, ev[2], ev[3]);
     cudaEventElapsedTime(&d, ev[3], ev[4]);
-    // The fused kernel computes responses and suppression together (and, in
-    // the two-launch plan, pyramid levels 1-2): its time is crf_us;
-    // pyramid_us is the separate downsampling launches; nms_us is the cell
+    // pyramid_us: the downsampling launches; the fused launches compute
+    // responses and suppression together (and, in the two-launch plan,
+    // pyramid levels 1-2): with stats their time is split by the kernel's
+    // phase cycles into crf_us (staging .. scoring) and nms_us (suppression,
+    // cell selection) plus the compaction, as frontend.cpp:42-53 times the
+    // two stages; without stats crf_us is the whole fused time and nms_us the
     // compaction.
-    if (fuse_pyr) {  // the pyramid is made inside the fused launches
-      times->pyramid_us = b * 1e3;
-      times->crf_us = (a + c) * 1e3;
-    } else {
-      times->pyramid_us = a * 1e3;
-      times->crf_us = c * 1e3;
-    }
+    const double fused = (fuse_pyr ? a + c : c) * 1e3;
+    times->pyramid_us = (fuse_pyr ? b : a) * 1e3;
+    times->crf_us = fused;
     times->nms_us = d * 1e3;
+    if (split) {
+      unsigned long long cyc[2] = {0, 0};
+      check_cuda(cudaMemcpy(cyc, d_phase_, sizeof(cyc), cudaMemcpyDeviceToHost), "phase cycles");
+      const double tot = static_cast<double>(cyc[0]) + static_cast<double>(cyc[1]);
+      if (tot > 0) {
+        times->crf_us = fused * static_cast<double>(cyc[0]) / tot;
+        times->nms_us += fused * static_cast<double>(cyc[1]) / tot;
+      }
+    }
     for (auto& e : ev) cudaEventDestroy(e);
   }
 }

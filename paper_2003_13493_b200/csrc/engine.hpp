@@ -158,6 +158,7 @@ class DeviceBatch {
   flk_feature* d_feats_ = nullptr;
   int* d_counts_ = nullptr;
   uint64_t* d_stats_ = nullptr;  // [capacity][2] = candidates, comparisons
+  unsigned long long* d_phase_ = nullptr;  // fused kernel phase cycles (timed stats runs)
   float* d_naive_ = nullptr;     // conformance scratch (lazily allocated)
   const void* fused_kern_ = nullptr;  // kernel the smem attribute below was set on
   size_t fused_smem_ = 0;        // dynamic shared memory of the fused kernel

@@ -125,6 +125,11 @@ struct Params {
   // columns (the reference's response values, 0 off corners and in the border)
   uint16_t* dbg_map;
   size_t dbg_fstride;
+  // stats path only: SM cycles spent by thread 0 of every CTA in the response
+  // phases (staging .. scoring) and in the suppression / selection phases,
+  // summed, so the host can split the fused launch's time like the
+  // reference's crf_us / nms_us (frontend.cpp:42-53)
+  unsigned long long* phase_cycles;
   // shared-memory layout and corner-list capacity, filled by the host
   // (finalize()) so the kernel does not recompute them
   int sm_stage, sm_planes, sm_cm, sm_list, sm_scan, sm_skeys, sm_bar, sm_xrow, cap;
@@ -410,6 +415,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_detect(const __grid_co
   const int slots = (cr1 - cr0 + 1) * P.cols;
   const bool local_keys = slots <= P.key_slots;
 
+  const long long t_start = P.phase_cycles && tid == 0 ? clock64() : 0;
   // --- 1. stage the rows [ya, yb), columns [max(bx0,0), ...) of this tile
   if (k > 0 && P.pdl_wait) asm volatile("griddepcontrol.wait;" ::: "memory");
   const uint8_t* frame = L.img + f * L.fstride;
@@ -838,6 +844,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_detect(const __grid_co
     }
   }
   __syncthreads();
+  const long long t_scored = P.phase_cycles && tid == 0 ? clock64() : 0;
   if (P.dbg_map) {  // diagnostic score dump (flkb_detector_fused_responses)
     uint16_t* out = P.dbg_map + f * P.dbg_fstride + L.dbg_off;
     const int tw = x_hi - x_lo;
@@ -1009,17 +1016,22 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_detect(const __grid_co
       atomicAdd(P.stats + 2 * f + 1, n_cmp);
     }
   }
-  if (!local_keys) return;
-  __syncthreads();
-
-  // --- 6. flush the shared cell keys into the frame's global keys
-  for (int i = tid; i < slots; i += kThreads) {
-    const uint32_t key = skeys[i];
-    if (!key) continue;
-    const int y = y0 + 1023 - static_cast<int>((key >> 10) & 1023u);
-    const int x = x_lo + 1023 - static_cast<int>(key & 1023u);
-    atomicMax(P.keys + static_cast<size_t>(f) * P.cells + i + cr0 * P.cols,
-              pack_key(static_cast<int>(key >> 20), k, x << k, y << k));
+  if (local_keys) {
+    __syncthreads();
+    // --- 6. flush the shared cell keys into the frame's global keys
+    for (int i = tid; i < slots; i += kThreads) {
+      const uint32_t key = skeys[i];
+      if (!key) continue;
+      const int y = y0 + 1023 - static_cast<int>((key >> 10) & 1023u);
+      const int x = x_lo + 1023 - static_cast<int>(key & 1023u);
+      atomicMax(P.keys + static_cast<size_t>(f) * P.cells + i + cr0 * P.cols,
+                pack_key(static_cast<int>(key >> 20), k, x << k, y << k));
+    }
+  }
+  if (P.phase_cycles && tid == 0) {
+    const long long t_end = clock64();
+    atomicAdd(P.phase_cycles, static_cast<unsigned long long>(t_scored - t_start));
+    atomicAdd(P.phase_cycles + 1, static_cast<unsigned long long>(t_end - t_scored));
   }
 }
 

@@ -159,3 +159,19 @@ def test_device_hypot_matches_glibc():
     g = fl.debug_hypot(pts[:, 0], pts[:, 1])
     w = np.array([libm.hypot(a, b) for a, b in pts.tolist()])
     assert ((g <= eps) == (w <= eps)).all() and (g == w).all()
+
+
+def test_stage_times_split_like_the_reference():
+    """flk_frame_stats (fastlk.h:106-119): pyramid_us, crf_us and nms_us are
+    all populated; the fused launch's time is split between crf_us (staging ..
+    scoring) and nms_us (suppression, cell selection, compaction) by the
+    kernel's own phase cycles, as frontend.cpp:42-53 times the two stages."""
+    img = synth.texture(7, 752, 480)
+    det = fl.Detector(_cfg())
+    for _ in range(3):
+        _, ex = det.run(img, stats=True)
+    st = ex["stats"]
+    assert st["pyramid_us"] > 0 and st["crf_us"] > 0 and st["nms_us"] > 0
+    assert st["track_us"] == 0
+    # suppression of ~100k candidates is a real share of the fused kernel
+    assert 0.05 < st["nms_us"] / (st["crf_us"] + st["nms_us"]) < 0.95

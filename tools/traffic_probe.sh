@@ -1,9 +1,9 @@
 #!/bin/bash
 # DRAM bytes of the k_detect launches of one C4 step per pyramid_chunk plan value
 mkdir -p gpurun_out
-for c in ${CHUNKS:-4096 512}; do
-  n=$(( 2 * (4096 + c - 1) / c ))
-  PYR_CHUNK=$c timeout 600 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,lts__t_bytes.sum \
+for c in ${CHUNKS:-0 4096 512}; do
+  if [ "$c" = 0 ]; then n=30; else n=$(( 2 * (4096 + c - 1) / c )); fi
+  PYR_CHUNK=$c timeout 600 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,lts__t_bytes.sum,smsp__inst_executed.sum,smsp__thread_inst_executed.sum \
     --cache-control none --clock-control none -k regex:k_detect -s $n -c $n --csv \
     --log-file gpurun_out/traffic_$c.csv python tools/traffic_probe.py > gpurun_out/traffic_$c.log 2>&1
   python - $c <<'PY'
