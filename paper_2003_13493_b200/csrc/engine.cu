@@ -289,7 +289,10 @@ fused::Params fused_geometry(const DetectParams& p, const Geometry& g, int R, in
     }
     L.div_nw = fused::FastDiv::make(static_cast<uint32_t>(L.nw));
     L.div_tiles = fused::FastDiv::make(static_cast<uint32_t>(L.tiles_x));
-    slots = std::max(slots, ((R << k) / p.cell_h + 2) * g.cols);
+    // in-CTA keys: the cell rows of R level-k rows x the cell columns of one
+    // tile's own columns
+    slots = std::max(slots, ((R << k) / p.cell_h + 2) *
+                                std::min(g.cols, ((L.tile_w << k) / p.cell_w + 2)));
   }
   P.nw_max = 1;
   for (int k = 0; k < g.levels; ++k) P.nw_max = std::max(P.nw_max, P.lv[k].nw);
@@ -453,7 +456,7 @@ void DeviceBatch::run(const uint8_t* frames, size_t fstride, int pitch, int coun
     return;
   }
   const bool fixed_pitch = p_.radius == 1 && P.sw == fused::kSw1 && P.rp == fused::kRp1;
-  const fused::KernelFn kern = fused::kernel_for(p_.arc_length, p_.score, fixed_pitch ? 1 : 0);
+  const fused::KernelFn kern = fused::kernel_for(p_.arc_length, p_.score, fixed_pitch ? 1 : 0, stats);
   if (reinterpret_cast<const void*>(kern) != fused_kern_ || static_cast<size_t>(smem) > fused_smem_) {
     check_cuda(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
                "fused smem attribute");

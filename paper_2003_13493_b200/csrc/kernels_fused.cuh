@@ -185,7 +185,7 @@ __host__ __device__ inline Smem smem_layout(const Params& p) {
   off += p.key_slots * 4;
   off = (off + 15) & ~15;
   s.bar = off;
-  off += 16;
+  off += 32;  // mbarrier + two phase-clock stamps
   s.total = off;
   return s;
 }
@@ -369,7 +369,10 @@ struct TaskIter {
   }
 };
 
-template <int N, int KIND, int RADIUS>
+// STATS: the counting instance (nms_candidates / nms_comparisons, phase
+// clocks), used only when flk_frame_stats are requested; the other instance
+// carries none of that code.
+template <int N, int KIND, int RADIUS, bool STATS>
 __global__ void __launch_bounds__(kThreads, kMinBlocks) k_detect(const __grid_constant__ Params P) {
   extern __shared__ __align__(128) uint8_t smem[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -410,12 +413,22 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_detect(const __grid_co
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + P.sm_bar);
 
   // cell rows touched by the suppressed rows [y0, y1) of level k
+  // and the cell columns of its own columns [x_lo, x_hi): the in-CTA keys
+  // cover only those cells
   const int cr0 = P.div_ch(y0 << k);
   const int cr1 = y1 > y0 ? P.div_ch((y1 - 1) << k) : cr0;
-  const int slots = (cr1 - cr0 + 1) * P.cols;
+#ifndef FLKB_TILE_SLOTS
+#define FLKB_TILE_SLOTS 1
+#endif
+  const int cc0 = FLKB_TILE_SLOTS ? P.div_cw(x_lo << k) : 0;
+  const int ccols = FLKB_TILE_SLOTS ? (x_hi > x_lo ? P.div_cw((x_hi - 1) << k) : cc0) - cc0 + 1 : P.cols;
+  const int slots = (cr1 - cr0 + 1) * ccols;
   const bool local_keys = slots <= P.key_slots;
 
-  const long long t_start = P.phase_cycles && tid == 0 ? clock64() : 0;
+  // phase clock (stats runs): thread 0 keeps its stamps in shared memory, so
+  // no register stays live across the kernel for them
+  long long* stamps = reinterpret_cast<long long*>(smem + P.sm_bar + 16);
+  if (STATS && P.phase_cycles && tid == 0) stamps[0] = clock64();
   // --- 1. stage the rows [ya, yb), columns [max(bx0,0), ...) of this tile
   if (k > 0 && P.pdl_wait) asm volatile("griddepcontrol.wait;" ::: "memory");
   const uint8_t* frame = L.img + f * L.fstride;
@@ -458,8 +471,10 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_detect(const __grid_co
       stage[(y - iy0) * SW + sx0 + x] = frame[static_cast<size_t>(y) * L.pitch + gx0 + x];
     }
   }
-  if (local_keys)
+  if (local_keys) {
+#pragma unroll 1
     for (int i = tid; i < slots; i += kThreads) skeys[i] = 0u;
+  }
   __syncthreads();
   if (L.tma || L.tmap_ok) {
     // row copies (one per thread, the barrier is armed) unless the tensor
@@ -844,7 +859,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_detect(const __grid_co
     }
   }
   __syncthreads();
-  const long long t_scored = P.phase_cycles && tid == 0 ? clock64() : 0;
+  if (STATS && P.phase_cycles && tid == 0) stamps[1] = clock64();
   if (P.dbg_map) {  // diagnostic score dump (flkb_detector_fused_responses)
     uint16_t* out = P.dbg_map + f * P.dbg_fstride + L.dbg_off;
     const int tw = x_hi - x_lo;
@@ -866,8 +881,8 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_detect(const __grid_co
     // cell map constants; the additive parts and the CTA's first cell row
     // fold into one base slot
     const uint32_t cmx = L.cmx, cmy = L.cmy;
-    uint32_t* const kbase = skeys + static_cast<int>(L.ccy - static_cast<uint32_t>(cr0)) * P.cols +
-                            static_cast<int>(L.ccx);
+    uint32_t* const kbase = skeys + static_cast<int>(L.ccy - static_cast<uint32_t>(cr0)) * ccols +
+                            static_cast<int>(L.ccx) - cc0;
     for (int w0 = e_lo; w0 < e_hi; w0 += cap) {
       const bool resident = total <= cap;  // the scoring list is still in place
       const int off = resident ? 0 : w0;
@@ -879,8 +894,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_detect(const __grid_co
       const int m_end = resident ? e_hi : min(w0 + cap, e_hi);
       // the loop is instantiated with and without the counters, so the
       // fast path carries no per-candidate stats test
-      auto suppress = [&](auto with_stats, auto local) {
-        constexpr bool STATS = decltype(with_stats)::value;
+      auto suppress = [&](auto local) {
         constexpr bool LOCAL = decltype(local)::value;
         for (int e = w0 + tid; e < m_end; e += kThreads) {
           const int ent = list[e - off];
@@ -941,7 +955,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_detect(const __grid_co
                                                       static_cast<uint32_t>(x)));
             const uint32_t cx = __umulhi(static_cast<uint32_t>(x), cmx);
             const uint32_t cy = __umulhi(static_cast<uint32_t>(y), cmy);
-            atomicMax(kbase + mad_fma(cy, static_cast<uint32_t>(P.cols), cx), key);
+            atomicMax(kbase + mad_fma(cy, static_cast<uint32_t>(ccols), cx), key);
           } else {
             const int X = x << k, Y = y << k;
             atomicMax(P.keys + static_cast<size_t>(f) * P.cells + P.div_ch(Y) * P.cols + P.div_cw(X),
@@ -956,7 +970,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_detect(const __grid_co
       // of the warp), FLKB_KEYS=2 is the paper's shfl_xor butterfly over
       // packed keys when every survivor of the warp falls in one cell
       // (per-lane atomics otherwise). Radius 1, shared keys, no counters.
-      if (!P.stats && RADIUS == 1 && local_keys) {
+      if (!STATS && RADIUS == 1 && local_keys) {
         for (int eb = w0 + warp * 32; eb < m_end; eb += kThreads) {  // warp-uniform trips
           const int e = eb + lane;
           uint32_t key = 0;
@@ -973,7 +987,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_detect(const __grid_co
               key = mad_fma(static_cast<uint32_t>(sc), P.pow2[20],
                             kc - mad_fma(static_cast<uint32_t>(y), P.pow2[10], static_cast<uint32_t>(x)));
               slot = static_cast<int>(mad_fma(__umulhi(static_cast<uint32_t>(y), cmy),
-                                              static_cast<uint32_t>(P.cols),
+                                              static_cast<uint32_t>(ccols),
                                               __umulhi(static_cast<uint32_t>(x), cmx)));
             }
           }
@@ -995,18 +1009,14 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_detect(const __grid_co
         }
       } else
 #endif
-      if (P.stats && local_keys)
-        suppress(std::true_type{}, std::true_type{});
-      else if (P.stats)
-        suppress(std::true_type{}, std::false_type{});
-      else if (local_keys)
-        suppress(std::false_type{}, std::true_type{});
+      if (local_keys)
+        suppress(std::true_type{});
       else
-        suppress(std::false_type{}, std::false_type{});
+        suppress(std::false_type{});
       if (resident) break;
     }
   }
-  if (P.stats) {
+  if (STATS) {
     for (int o = 16; o; o >>= 1) {
       n_cand += __shfl_xor_sync(0xffffffffu, n_cand, o);
       n_cmp += __shfl_xor_sync(0xffffffffu, n_cmp, o);
@@ -1016,23 +1026,35 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_detect(const __grid_co
       atomicAdd(P.stats + 2 * f + 1, n_cmp);
     }
   }
-  if (local_keys) {
-    __syncthreads();
-    // --- 6. flush the shared cell keys into the frame's global keys
-    for (int i = tid; i < slots; i += kThreads) {
-      const uint32_t key = skeys[i];
-      if (!key) continue;
-      const int y = y0 + 1023 - static_cast<int>((key >> 10) & 1023u);
-      const int x = x_lo + 1023 - static_cast<int>(key & 1023u);
-      atomicMax(P.keys + static_cast<size_t>(f) * P.cells + i + cr0 * P.cols,
-                pack_key(static_cast<int>(key >> 20), k, x << k, y << k));
+  // phase clock (stats runs only)
+  auto phase_end = [&] {
+    if (STATS && P.phase_cycles && tid == 0) {
+      const long long t_end = clock64();
+      atomicAdd(P.phase_cycles, static_cast<unsigned long long>(stamps[1] - stamps[0]));
+      atomicAdd(P.phase_cycles + 1, static_cast<unsigned long long>(t_end - stamps[1]));
     }
+  };
+  if (!local_keys) {
+    phase_end();
+    return;
   }
-  if (P.phase_cycles && tid == 0) {
-    const long long t_end = clock64();
-    atomicAdd(P.phase_cycles, static_cast<unsigned long long>(t_scored - t_start));
-    atomicAdd(P.phase_cycles + 1, static_cast<unsigned long long>(t_end - t_scored));
+  __syncthreads();
+
+  // --- 6. flush the shared cell keys into the frame's global keys
+  const float inv_cc = 1.0f / static_cast<float>(ccols);
+#pragma unroll 1
+  for (int i = tid; i < slots; i += kThreads) {
+    const uint32_t key = skeys[i];
+    if (!key) continue;
+    // slot row i / ccols: (i + 1/2) / ccols is at least 1/(2 ccols) from an
+    // integer, far more than the float error for i < 2^16
+    const int rr = __float2int_rz((static_cast<float>(i) + 0.5f) * inv_cc);
+    const int y = y0 + 1023 - static_cast<int>((key >> 10) & 1023u);
+    const int x = x_lo + 1023 - static_cast<int>(key & 1023u);
+    atomicMax(P.keys + static_cast<size_t>(f) * P.cells + (cr0 + rr) * P.cols + cc0 + (i - rr * ccols),
+              pack_key(static_cast<int>(key >> 20), k, x << k, y << k));
   }
+  phase_end();
 }
 
 }  // namespace fused
