@@ -341,6 +341,12 @@ class BatchPipeline {
       drain(sl, outs);
       const int cnt = std::min(kChunk, n - c0);
       uint8_t* hp = static_cast<uint8_t*>(sl.in.p);
+      // the chunk's frames as one batched copy submission (one API call for
+      // up to kChunk page-locked sources), per-frame copies where the runtime
+      // has no batch copies
+      void* dsts[kChunk];
+      void* srcs[kChunk];
+      size_t sizes[kChunk];
       for (int j = 0; j < cnt; ++j) {
         const flkb::HostImage& img = images[c0 + j]->img;
         const uint8_t* src = img.px.data();
@@ -350,9 +356,29 @@ class BatchPipeline {
             std::memcpy(dst + static_cast<size_t>(y) * pitch_, src + static_cast<size_t>(y) * w_, w_);
           src = dst;
         }
-        flkb::check_cuda(cudaMemcpyAsync(sl.d_in + static_cast<size_t>(j) * fs_, src, fs_,
-                                         cudaMemcpyHostToDevice, sl.s), "H2D batch frame");
+        dsts[j] = sl.d_in + static_cast<size_t>(j) * fs_;
+        srcs[j] = const_cast<uint8_t*>(src);
+        sizes[j] = fs_;
       }
+      bool batched = false;
+      if (batch_copies_) {
+        cudaMemcpyAttributes attr{};
+        attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
+        attr.srcLocHint.type = cudaMemLocationTypeHost;
+        attr.dstLocHint.type = cudaMemLocationTypeDevice;
+        attr.dstLocHint.id = device_;
+        attr.flags = cudaMemcpyFlagPreferOverlapWithCompute;
+        size_t idx0 = 0, fail = 0;
+        batched = cudaMemcpyBatchAsync(dsts, srcs, sizes, static_cast<size_t>(cnt), &attr, &idx0, 1,
+                                       &fail, sl.s) == cudaSuccess;
+        if (!batched) {
+          cudaGetLastError();
+          batch_copies_ = false;  // this runtime / driver has none: per-frame copies from now on
+        }
+      }
+      for (int j = 0; !batched && j < cnt; ++j)
+        flkb::check_cuda(cudaMemcpyAsync(dsts[j], srcs[j], sizes[j], cudaMemcpyHostToDevice, sl.s),
+                         "H2D batch frame");
       sl.b->run(sl.d_in, fs_, pitch_, cnt, false, sl.s);
       sl.b->download(0, cnt, static_cast<int*>(sl.out.p), results(sl), sl.s);
       sl.first = c0;
@@ -389,6 +415,7 @@ class BatchPipeline {
 
   int device_, w_, h_, pitch_ = 0, cells_ = 0;
   size_t fs_ = 0;
+  bool batch_copies_ = true;
   Slot slots_[2];
 };
 

@@ -37,8 +37,9 @@ def main():
         assert (feats == ref).all() and extra["stats"]["nms_comparisons"] == st.comparisons
         assert (det.run(img) == ref).all()
         maps = det.responses(img, cfg["l"])
-        for a, b in zip(maps, orc.responses(img, oracle.make_params(**cfg))):
-            assert (a == b).all()
+        fmaps = det.responses(img, cfg["l"], fused=True)  # the fused kernel's own score tiles
+        for a, b, c in zip(maps, fmaps, orc.responses(img, oracle.make_params(**cfg))):
+            assert (a == c).all() and (b == c).all()
     img = synth.noise(5, 200, 120)  # multi-round corner lists
     cfg = dict(epsilon=0, N=9, score_kind="sad_b", l=2, w=1, h=16, n=1)
     feats = fl.Detector(fl.Config(**cfg), plan={"list_cap": 256}).run(img)
@@ -59,6 +60,11 @@ def main():
         assert (res[f] == orc.detect(synth.texture(40 + f, W, H), oracle.make_params(**cfg))[0]).all()
     total, _ = batch.conformance(d.data_ptr(), W * H, W, 0, n)
     assert total["false_positives"] == 0 and total["matched"] == sum(len(r) for r in res)
+    # host batches through the multi-device entry point (device 0 twice)
+    hb = [synth.texture(60 + f, 256, 160) for f in range(5)]
+    d2 = fl.Detector(fl.Config(**cfg))
+    for a, b in zip(d2.run_batch_multi(hb, [0, 0]), fl.Detector(fl.Config(**cfg)).run_batch(hb)):
+        assert (a == b).all()
     frames = sessions.drifting_sequence(3, 192, 128)
     scfg = dict(epsilon=10, N=9, score_kind="sad_b", l=2, w=1, h=16, n=1, target_count=12,
                 redetect_ratio=0.5, param_mode="full", max_iterations=30, convergence_epsilon=0.01)
