@@ -306,6 +306,7 @@ fused::Params fused_geometry(const DetectParams& p, const Geometry& g, int R, in
   P.key_slots = slots <= 4096 ? slots : 0;
   for (int i = 0; i < 32; ++i) P.pow2[i] = 1u << i;
   for (int b = 0; b < 8; ++b) P.emask[b] = ((p.epsilon >> b) & 1) ? 0xFFFFFFFFu : 0u;
+  P.neg16eps = 0u - 16u * static_cast<uint32_t>(p.epsilon);
   P.list_cap = p.plan.list_cap;
   return P;
 }

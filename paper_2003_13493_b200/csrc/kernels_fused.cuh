@@ -119,6 +119,7 @@ struct Params {
   int list_cap;   // corner-list capacity (0 = 24 entries per thread)
   uint32_t pow2[32];  // 1 << i, read from the constant bank so shifts can issue as IMAD
   uint32_t emask[8];  // ~0 where bit b of eps is set
+  uint32_t neg16eps;  // -16 eps mod 2^32 (SAD-B)
   unsigned long long* keys;
   unsigned long long* stats;
   // diagnostic: when set, every CTA writes the u16 scores of its own rows and
@@ -335,16 +336,18 @@ __device__ __forceinline__ uint32_t vabsdiff4_acc(uint32_t a, uint32_t b, uint32
 
 // SAD-B of one corner from its 16 ring bytes packed 4 per word:
 // sum max(|d|-e,0) = (sum | |d| - e | + sum |d| - 16 e) / 2.
-__device__ __forceinline__ int sad_b_packed(const uint32_t (&r)[4], uint32_t c, uint32_t eps) {
+// acc0 = -16 e (mod 2^32), a constant-bank operand, starts the first sum.
+__device__ __forceinline__ int sad_b_packed(const uint32_t (&r)[4], uint32_t c, uint32_t eps,
+                                            uint32_t acc0) {
   const uint32_t c4 = c * 0x01010101u, e4 = eps * 0x01010101u;
-  uint32_t acc1 = 0, acc2 = 0;
+  uint32_t acc1 = acc0, acc2 = 0;
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
     const uint32_t d = __vabsdiffu4(r[k], c4);
     acc1 = vabsdiff4_acc(d, e4, acc1);
     acc2 = vabsdiff4_acc(r[k], c4, acc2);
   }
-  return static_cast<int>((acc1 + acc2 - 16u * eps) >> 1);
+  return static_cast<int>((acc1 + acc2) >> 1);
 }
 
 // ---------------------------------------------------------------- kernel
@@ -848,7 +851,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_detect(const __grid_co
         for (int q = 0; q < 4; ++q)  // bytes packed with IMAD (FMA pipe; the ALU pipe is the busy one)
           pk[q] = mad_fma(rb[4 * q + 3], P.pow2[24],
                           mad_fma(rb[4 * q + 2], P.pow2[16], mad_fma(rb[4 * q + 1], P.pow2[8], rb[4 * q])));
-        sc = sad_b_packed(pk, cc, static_cast<uint32_t>(P.eps));
+        sc = sad_b_packed(pk, cc, static_cast<uint32_t>(P.eps), P.neg16eps);
       } else {
         int ring[16];
 #pragma unroll
@@ -874,6 +877,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_detect(const __grid_co
   unsigned long long n_cand = 0, n_cmp = 0;
   {
     const int nx_lo = max(x_lo, 3), nx_hi = min(x_hi, w - 3);
+    const unsigned nspan = nx_hi > nx_lo ? static_cast<unsigned>(nx_hi - nx_lo) : 0u;
     const int e_lo = T1 > T0 ? scan[kWarps + 1] : 0;
     const int e_hi = T1 > T0 ? scan[kWarps + 2] : 0;
     const int rp = RP;
@@ -900,7 +904,8 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_detect(const __grid_co
           const int ent = list[e - off];
           const int y = cy_lo + (ent >> 10), xs = ent & 1023;
           const int x = bx0 + xs;
-          if (x < nx_lo || x >= nx_hi) continue;  // halo column of a neighbouring tile
+          // halo column of a neighbouring tile (one unsigned range test)
+          if (static_cast<unsigned>(x - nx_lo) >= nspan) continue;
           const uint16_t* row = tile_s + (y - fy0) * rp + xs + tcol;
           const int s = row[0];
           // a corner whose score is 0 (MT, eps 0) is no candidate; a SAD score
