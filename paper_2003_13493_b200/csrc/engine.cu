@@ -245,6 +245,38 @@ bool encode_stage_map(fused::Level& L, int frames, int box_w, int box_h) {
              CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// The launch's per-CTA geometry table (fused::Params::geo): level, rows,
+// columns and in-CTA cell range of each CTA, packed in 16-bit fields; empty
+// (the kernel computes its own) when the launch has more CTAs than the table
+// holds or a field does not fit.
+void fill_geometry(fused::Params& P, int kb, int ke, int ctas) {
+  P.geo_n = 0;
+  if (ctas > fused::kGeoMax) return;
+  int i = 0;
+  for (int k = kb; k < ke; ++k) {
+    const fused::Level& L = P.lv[k];
+    for (int local = 0; local < L.bands * L.tiles_x; ++local, ++i) {
+      const int band = local / L.tiles_x, tile = local % L.tiles_x;
+      const int y0 = band * P.R, y1 = std::min(y0 + P.R, L.h);
+      const int x_lo = tile * L.tile_w, x_hi = std::min(x_lo + L.tile_w, L.w);
+      const int cr0 = (y0 << k) / P.cell_h;
+      const int nrows = (y1 > y0 ? ((y1 - 1) << k) / P.cell_h : cr0) - cr0 + 1;
+      const int cc0 = (x_lo << k) / P.cell_w;
+      const int ccols = (x_hi > x_lo ? ((x_hi - 1) << k) / P.cell_w : cc0) - cc0 + 1;
+      const int v[8] = {y0, y1, x_lo, x_hi, cr0, cc0, ccols, nrows};
+      for (int x : v)
+        if (x < 0 || x > 0xFFFF) return;
+      if (k > 15 || nrows > 4095) return;
+      P.geo[i] = make_uint4(static_cast<uint32_t>(k) | static_cast<uint32_t>(nrows) << 4 |
+                                static_cast<uint32_t>(y0) << 16,
+                            static_cast<uint32_t>(y1) | static_cast<uint32_t>(x_lo) << 16,
+                            static_cast<uint32_t>(x_hi) | static_cast<uint32_t>(cr0) << 16,
+                            static_cast<uint32_t>(cc0) | static_cast<uint32_t>(ccols) << 16);
+    }
+  }
+  P.geo_n = ctas;
+}
+
 // kMinBlocks CTAs per SM (1 KB of each CTA's share is reserved by the driver)
 constexpr int kFusedSmemTarget = (228 * 1024) / fused::kMinBlocks - 1024;
 constexpr int kFusedSmemMax = 227 * 1024;
@@ -526,6 +558,7 @@ void DeviceBatch::run(const uint8_t* frames, size_t fstride, int pitch, int coun
       P.lv[k].cta0 = ctas;
       ctas += P.lv[k].bands * P.lv[k].tiles_x;
     }
+    fill_geometry(P, kb, ke, ctas);
     if (P.pdl_wait) {  // overlap the pyramid kernel (and this launch's latency)
       cudaLaunchConfig_t lc{};
       lc.gridDim = dim3(ctas, n);

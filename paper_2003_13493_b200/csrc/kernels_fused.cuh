@@ -53,6 +53,7 @@ constexpr int kMinBlocks = FLKB_MIN_BLOCKS;
 #define FLKB_KEYS 0
 #endif  // CTAs per SM the register budget targets
 constexpr int kMaxLv = 16;
+constexpr int kGeoMax = 64;  // CTA geometry entries carried in the launch parameters (1 KB)
 // Stage pitch (bytes) and score-tile pitch (u16) of the radius-1 instance:
 // column tiles up to 192 px (8 plane words) fit them.
 constexpr int kSw1 = 224;
@@ -134,6 +135,11 @@ struct Params {
   // shared-memory layout and corner-list capacity, filled by the host
   // (finalize()) so the kernel does not recompute them
   int sm_stage, sm_planes, sm_cm, sm_list, sm_scan, sm_skeys, sm_bar, sm_xrow, cap;
+  // per-CTA geometry of this launch (host table, geo_n entries; CTAs past it
+  // compute theirs): x = k | (cell rows) << 4 | y0 << 16, y = y1 | x_lo << 16,
+  // z = x_hi | first cell row << 16, w = first cell column | cell columns << 16
+  int geo_n;
+  uint4 geo[kGeoMax];
 };
 
 struct Smem {
@@ -385,16 +391,41 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_detect(const __grid_co
   const int SW = RADIUS == 1 ? kSw1 : P.sw;
   const int RP = RADIUS == 1 ? kRp1 : P.rp;
 
-  // --- which level, band and column tile
-  int k = P.k_begin;
-  while (k + 1 < P.k_end && static_cast<int>(blockIdx.x) >= P.lv[k + 1].cta0) ++k;
+  // --- which level, band and column tile: from the host's table of this
+  //     launch's CTAs (level, rows, columns, cell range), else computed
+  int k, y0, y1, x_lo, x_hi, cr0, nrows, cc0, ccols;
+  if (static_cast<int>(blockIdx.x) < P.geo_n) {
+    const uint4 g = P.geo[blockIdx.x];
+    k = g.x & 15u;
+    nrows = (g.x >> 4) & 4095u;
+    y0 = g.x >> 16;
+    y1 = g.y & 0xFFFFu;
+    x_lo = g.y >> 16;
+    x_hi = g.z & 0xFFFFu;
+    cr0 = g.z >> 16;
+    cc0 = g.w & 0xFFFFu;
+    ccols = g.w >> 16;
+  } else {
+    k = P.k_begin;
+    while (k + 1 < P.k_end && static_cast<int>(blockIdx.x) >= P.lv[k + 1].cta0) ++k;
+    const Level& Lk = P.lv[k];
+    const int local = blockIdx.x - Lk.cta0;
+    const int band = Lk.div_tiles(local), tile = local - band * Lk.tiles_x;
+    y0 = band * P.R;
+    y1 = min(y0 + P.R, Lk.h);
+    x_lo = tile * Lk.tile_w;
+    x_hi = min(x_lo + Lk.tile_w, Lk.w);
+    // cell rows touched by the suppressed rows [y0, y1) of level k and the
+    // cell columns of its own columns [x_lo, x_hi): the in-CTA keys cover
+    // only those cells
+    cr0 = P.div_ch(y0 << k);
+    nrows = (y1 > y0 ? P.div_ch((y1 - 1) << k) : cr0) - cr0 + 1;
+    cc0 = P.div_cw(x_lo << k);
+    ccols = (x_hi > x_lo ? P.div_cw((x_hi - 1) << k) : cc0) - cc0 + 1;
+  }
   const Level& L = P.lv[k];
-  const int local = blockIdx.x - L.cta0;
-  const int band = L.div_tiles(local), tile = local - band * L.tiles_x;
   const int f = blockIdx.y;
   const int n = RADIUS > 0 ? RADIUS : P.radius, w = L.w, h = L.h;
-  const int y0 = band * P.R, y1 = min(y0 + P.R, h);          // rows suppressed here
-  const int x_lo = tile * L.tile_w, x_hi = min(x_lo + L.tile_w, w);
   const int fy0 = y0 - n;                                       // tile row 0 <-> image row fy0
   const int iy0 = fy0 - 3;                                      // stage row 0 <-> image row iy0
   const int ya = max(iy0, 0), yb = min(y1 + n + 3, h);          // rows present in the stage
@@ -415,17 +446,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_detect(const __grid_co
   uint32_t* skeys = reinterpret_cast<uint32_t*>(smem + P.sm_skeys);
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + P.sm_bar);
 
-  // cell rows touched by the suppressed rows [y0, y1) of level k
-  // and the cell columns of its own columns [x_lo, x_hi): the in-CTA keys
-  // cover only those cells
-  const int cr0 = P.div_ch(y0 << k);
-  const int cr1 = y1 > y0 ? P.div_ch((y1 - 1) << k) : cr0;
-#ifndef FLKB_TILE_SLOTS
-#define FLKB_TILE_SLOTS 1
-#endif
-  const int cc0 = FLKB_TILE_SLOTS ? P.div_cw(x_lo << k) : 0;
-  const int ccols = FLKB_TILE_SLOTS ? (x_hi > x_lo ? P.div_cw((x_hi - 1) << k) : cc0) - cc0 + 1 : P.cols;
-  const int slots = (cr1 - cr0 + 1) * ccols;
+  const int slots = nrows * ccols;
   const bool local_keys = slots <= P.key_slots;
 
   // phase clock (stats runs): thread 0 keeps its stamps in shared memory, so
