@@ -59,7 +59,9 @@ FLK_API flk_status flkb_detector_run_batch_multi(flk_detector* detector, const i
  * "pyramid_chunk" (frames, 0 = auto), "pdl" (0/1), "list_cap" (corner-list
  * entries, 0 = auto), "debug_geom" (0/1), "staged" (1: the staged v1 kernels, one
  * launch per stage and level with u16 score maps in HBM -- the design
- * baseline the fused kernel is measured against). Results never depend on
+ * baseline the fused kernel is measured against), "batch_copies" (0: host
+ * batches copy frame by frame instead of one cudaMemcpyBatchAsync per chunk).
+ * Results never depend on
  * the plan.
  * Setting a detector's plan drops its cached device workspaces; batches take
  * the detector's plan at creation. Unknown key: FLK_E_CONFIG. */

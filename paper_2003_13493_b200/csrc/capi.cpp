@@ -302,7 +302,7 @@ class BatchPipeline {
  public:
   static constexpr int kChunk = 128;
   BatchPipeline(const flkb::DetectParams& p, int device, int w, int h)
-      : device_(device), w_(w), h_(h) {
+      : device_(device), w_(w), h_(h), batch_copies_(p.plan.batch_copies != 0) {
     flkb::DeviceGuard guard(device_);
     pitch_ = static_cast<int>(round16(static_cast<size_t>(w)));
     fs_ = static_cast<size_t>(pitch_) * h;
@@ -415,7 +415,7 @@ class BatchPipeline {
 
   int device_, w_, h_, pitch_ = 0, cells_ = 0;
   size_t fs_ = 0;
-  bool batch_copies_ = true;
+  bool batch_copies_;
   Slot slots_[2];
 };
 

@@ -86,6 +86,7 @@ bool LaunchPlan::set(const std::string& key, int value) {
   else if (key == "debug_geom") debug_geom = value != 0;
   else if (key == "staged") staged = value != 0;
   else if (key == "tensor_tma") tensor_tma = value != 0;
+  else if (key == "batch_copies") batch_copies = value != 0;
   else return false;
   return true;
 }

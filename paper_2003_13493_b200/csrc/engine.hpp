@@ -40,6 +40,7 @@ struct LaunchPlan {
   int debug_geom = 0;     // print the chosen shape to stderr
   int staged = 0;         // 1: the staged v1 kernels (one launch per stage and level, u16 maps in HBM)
   int tensor_tma = 1;     // stage each CTA's rows with one tensor-map TMA copy (0: one bulk copy per row)
+  int batch_copies = 1;   // host batches: one cudaMemcpyBatchAsync per chunk (0: per-frame copies)
   // key = value setter; false for an unknown key
   bool set(const std::string& key, int value);
 };

@@ -53,6 +53,14 @@ constexpr int kMinBlocks = FLKB_MIN_BLOCKS;
 #define FLKB_KEYS 0
 #endif  // CTAs per SM the register budget targets
 constexpr int kMaxLv = 16;
+#ifndef FLKB_SCORE_UNROLL
+#define FLKB_SCORE_UNROLL 1
+#endif
+#ifndef FLKB_NMS_UNROLL
+#define FLKB_NMS_UNROLL 1
+#endif
+constexpr int kScoreUnroll = FLKB_SCORE_UNROLL;  // scoring / suppression loop unroll (A/B knobs)
+constexpr int kNmsUnroll = FLKB_NMS_UNROLL;
 constexpr int kGeoMax = 64;  // CTA geometry entries carried in the launch parameters (1 KB)
 // Stage pitch (bytes) and score-tile pitch (u16) of the radius-1 instance:
 // column tiles up to 192 px (8 plane words) fit them.
@@ -857,6 +865,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_detect(const __grid_co
     build(w0);
     __syncthreads();
     const int m_end = min(cap, total - w0);
+#pragma unroll kScoreUnroll
     for (int e = tid; e < m_end; e += kThreads) {
       const int ent = list[e];
       const int y = cy_lo + (ent >> 10), xs = ent & 1023;
@@ -921,6 +930,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_detect(const __grid_co
       // fast path carries no per-candidate stats test
       auto suppress = [&](auto local) {
         constexpr bool LOCAL = decltype(local)::value;
+#pragma unroll kNmsUnroll
         for (int e = w0 + tid; e < m_end; e += kThreads) {
           const int ent = list[e - off];
           const int y = cy_lo + (ent >> 10), xs = ent & 1023;

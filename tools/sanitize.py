@@ -62,8 +62,12 @@ def main():
     assert total["false_positives"] == 0 and total["matched"] == sum(len(r) for r in res)
     # host batches through the multi-device entry point (device 0 twice)
     hb = [synth.texture(60 + f, 256, 160) for f in range(5)]
-    d2 = fl.Detector(fl.Config(**cfg))
-    for a, b in zip(d2.run_batch_multi(hb, [0, 0]), fl.Detector(fl.Config(**cfg)).run_batch(hb)):
+    # initcheck does not follow cudaMemcpyBatchAsync (tools/probes/batchcopy_initcheck.cu):
+    # under it (SANITIZE_TOOL=initcheck) the host batches copy frame by frame
+    per_frame = os.environ.get("SANITIZE_TOOL") == "initcheck"
+    d2 = fl.Detector(fl.Config(**cfg), plan={"batch_copies": 0} if per_frame else None)
+    d1 = fl.Detector(fl.Config(**cfg), plan={"batch_copies": 0} if per_frame else None)
+    for a, b in zip(d2.run_batch_multi(hb, [0, 0]), d1.run_batch(hb)):
         assert (a == b).all()
     frames = sessions.drifting_sequence(3, 192, 128)
     scfg = dict(epsilon=10, N=9, score_kind="sad_b", l=2, w=1, h=16, n=1, target_count=12,
