@@ -302,8 +302,8 @@ fused::Params fused_geometry(const DetectParams& p, const Geometry& g, int R, in
     fused::Level& L = P.lv[k];
     L.w = g.lw[k];
     L.h = g.lh[k];
-    // every level uses level 0's tile width; u16 corner-list entries address
-    // stage columns below 1024, so tiles are at most 928 px
+    // every level uses level 0's tile width; u16 corner-list entries are
+    // score-tile indices ((R + 2 radius) rows <= 64 of tiles up to 928 px)
     const int tw0 = std::min((g.lw[0] + tiles0 - 1) / tiles0, 928);
     L.tiles_x = (L.w + tw0 - 1) / tw0;
     L.tile_w = (L.w + L.tiles_x - 1) / L.tiles_x;
@@ -334,6 +334,7 @@ fused::Params fused_geometry(const DetectParams& p, const Geometry& g, int R, in
   P.rp = static_cast<int>(round_up(static_cast<size_t>(tw_max + 4 * n), 8));
   // the radius-1 instance has compile-time pitches; layouts that fit are padded to them
   if (n == 1 && P.sw <= fused::kSw1 && P.rp <= fused::kRp1) P.sw = fused::kSw1, P.rp = fused::kRp1;
+  P.rp_magic = 0xFFFFFFFFu / static_cast<uint32_t>(P.rp) + 1u;  // ceil(2^32 / rp)
   // 32-bit in-cell keys need cells of at most 1024 px per side
   // 32-bit in-CTA keys (score << 20 | 10-bit y and x offsets inside the CTA)
   P.key_slots = slots <= 4096 ? slots : 0;
@@ -396,7 +397,7 @@ void DeviceBatch::run(const uint8_t* frames, size_t fstride, int pitch, int coun
   const int r_min = 8;
   const LaunchPlan& plan = p_.plan;
   const bool forced = plan.band_rows > 0;  // tuning / test override
-  // u16 corner-list entries hold the band row in 6 bits: R + 2 radius <= 64
+  // u16 corner-list entries are score-tile indices: R + 2 radius <= 64
   const int r_max = std::max(4, (64 - 2 * p_.radius) & ~3);
   if (forced) R = std::min(r_max, std::max(4, plan.band_rows));
   const bool forced_tiles = plan.tiles > 0;  // tuning / test override
@@ -478,7 +479,9 @@ void DeviceBatch::run(const uint8_t* frames, size_t fstride, int pitch, int coun
   if (plan.debug_geom)
     std::fprintf(stderr, "flkb: R=%d tiles0=%d smem=%d ctas=%d\n", R, tiles0, smem, ctas_of(P));
   // pathological radius (or the staged plan asked for): the staged kernels
-  if (smem > kFusedSmemMax || R + 2 * p_.radius > 64 || plan.staged) {
+  // (corner-list entries are u16 score-tile indices: (R + 2 radius) rows x rp)
+  if (smem > kFusedSmemMax || R + 2 * p_.radius > 64 || (R + 2 * p_.radius) * P.rp > 65536 ||
+      plan.staged) {
     run_staged(frames, fstride, pitch, count, stats, s, times, first);
     if (out_counts)
       check_cuda(cudaMemcpyAsync(out_counts, d_counts_ + first, sizeof(int) * count,

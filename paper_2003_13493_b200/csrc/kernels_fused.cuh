@@ -66,6 +66,7 @@ constexpr int kGeoMax = 64;  // CTA geometry entries carried in the launch param
 // column tiles up to 192 px (8 plane words) fit them.
 constexpr int kSw1 = 224;
 constexpr int kRp1 = 200;
+constexpr uint32_t kRpMagic1 = 0xFFFFFFFFu / kRp1 + 1u;  // ceil(2^32 / 200)
 
 // Exact x / d for 0 <= x < 2^31 with one IMAD.HI: q = (umulhi(x, m) + x) >> l,
 // l = ceil(log2 d), m = 1 + floor(2^32 (2^l - d) / d).
@@ -124,6 +125,7 @@ struct Params {
   int sw;         // stage row pitch (bytes)
   int nw_max;     // plane words per row, max over tiles
   int rp;         // score tile pitch (u16)
+  uint32_t rp_magic;  // ceil(2^32 / rp): tile row of a tile index e < 2^16 is umulhi(e, rp_magic)
   int key_slots;  // shared cell-key capacity
   int list_cap;   // corner-list capacity (0 = 24 entries per thread)
   uint32_t pow2[32];  // 1 << i, read from the constant bank so shifts can issue as IMAD
@@ -327,6 +329,20 @@ __device__ __forceinline__ uint32_t sliced_arc(const uint32_t (&m)[16]) {
   uint32_t w3[16], w9[16];
 #pragma unroll
   for (int i = 0; i < 16; ++i) w3[i] = and3(m[i], m[(i + 1) & 15], m[(i + 2) & 15]);
+  if (N == 9) {
+    // runs of 9 start at i: T_i = w3[i] & w3[i+3] & w3[i+6]; two starts 3
+    // apart share two factors, T_i | T_{i+3} = w3[i+3] & w3[i+6] & (w3[i] |
+    // w3[i+9]), and the starts pair up along the 16-cycle i -> i+3 (gcd(3,16)
+    // = 1): two LOP3 per pair instead of two AND3 and an OR
+    uint32_t t[8];
+    constexpr int kPair[8] = {0, 6, 12, 2, 8, 14, 4, 10};
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int i = kPair[q];
+      t[q] = and3(w3[(i + 3) & 15], w3[(i + 6) & 15], w3[i] | w3[(i + 9) & 15]);
+    }
+    return or3(or3(t[0], t[1], t[2]), or3(t[3], t[4], t[5]), t[6] | t[7]);
+  }
 #pragma unroll
   for (int i = 0; i < 16; ++i) w9[i] = and3(w3[i], w3[(i + 3) & 15], w3[(i + 6) & 15]);
   if (N > 9) {
@@ -737,7 +753,10 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_detect(const __grid_co
 
   // --- 4. one CTA-wide corner list (row-major task order) from a block scan
   //        of per-task corner counts; the score tile (aliasing the dead
-  //        planes) is zeroed meanwhile. Entries: (row - cy_lo) << 10 | stage column.
+  //        planes) is zeroed meanwhile. An entry is the corner's index in the
+  //        score tile, (y - fy0) * RP + (x - x_lo + 2n): the tile store takes it
+  //        as is, the stage address is one IMAD.HI + one IMAD away, and the
+  //        order of entries is the (y, x) order the in-CTA keys rank by.
   const int tasks_f = max(fast_rows, 0) * nw;
   const int per = (tasks_f + kThreads - 1) / kThreads;
   const int tb = min(tid * per, tasks_f), te = min(tb + per, tasks_f);
@@ -784,6 +803,14 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_detect(const __grid_co
   if (pre1 >= 0) scan[kWarps + 2] = base + pre1;
   const int cap = P.cap;
   const int row_tb = L.div_nw(tb), j_tb = tb - row_tb * nw;
+  // Score-tile column of stage column xs: xs + bx0 - (x_lo - 2n), i.e. an n-wide
+  // zero margin left of the FAST columns.
+  const int tcol = bx0 - (x_lo - 2 * n);
+  // entry of bit 0 of task tb's word: tile row (row_tb + cy_lo - fy0), tile
+  // column kOwn * j_tb + tcol; the next word of a row is kOwn further, a row
+  // wrap adds RP - kOwn * nw
+  const uint32_t eb_tb = static_cast<uint32_t>((row_tb + cy_lo - fy0) * RP + kOwn * j_tb + tcol);
+  const uint32_t e_wrap = static_cast<uint32_t>(RP - kOwn * nw);
   // Writes the entries with list index in [w0, w0 + cap) to list[index - w0].
   auto build = [&](int w0) {
     if (total <= cap) {
@@ -791,11 +818,11 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_detect(const __grid_co
       // lane walk its own bits (cost ~ max popc) or expands the non-empty words
       // one at a time across the lanes (cost ~ non-empty words), whichever is
       // cheaper for this slot.
-      int pos = base, row = row_tb, j = j_tb;
+      int pos = base, j = j_tb;
+      uint32_t e0 = eb_tb;
       for (int q = 0; q < per; ++q) {
         const int t = tb + q;
         uint32_t m = t < te ? cm[t] : 0u;
-        const uint32_t e0 = (static_cast<uint32_t>(row) << 10) | static_cast<uint32_t>(kOwn * j);
         const int c = __popc(m);
         const unsigned nz = __ballot_sync(0xffffffffu, m != 0u);
         const int mx = __reduce_max_sync(0xffffffffu, c);
@@ -833,33 +860,37 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_detect(const __grid_co
           }
         }
         pos += c;
+        e0 += kOwn;
         if (++j == nw) {
           j = 0;
-          ++row;
+          e0 += e_wrap;
         }
       }
       return;
     }
     if (base >= w0 + cap || base + cnt <= w0) return;
-    int pos = base, row = row_tb, j = j_tb;
+    int pos = base, j = j_tb;
+    uint32_t e0 = eb_tb;
     for (int t = tb; t < te; ++t) {
       uint32_t m = cm[t];
-      const uint32_t e0 = (static_cast<uint32_t>(row) << 10) | static_cast<uint32_t>(kOwn * j);
       while (m) {
         const int b = __ffs(m) - 1;
         m &= m - 1;
         if (pos >= w0 && pos < w0 + cap) list[pos - w0] = static_cast<uint16_t>(e0 + b);
         ++pos;
       }
+      e0 += kOwn;
       if (++j == nw) {
         j = 0;
-        ++row;
+        e0 += e_wrap;
       }
     }
   };
-  // Score-tile column of stage column xs: xs + bx0 - (x_lo - 2n), i.e. an n-wide
-  // zero margin left of the FAST columns.
-  const int tcol = bx0 - (x_lo - 2 * n);
+  // tile row of an entry: one IMAD.HI (exact for entries < 2^16)
+  const uint32_t rp_magic = RADIUS == 1 ? kRpMagic1 : P.rp_magic;
+  // stage byte of tile index 0's pixel: stage row 3 (tile row 0 = image row
+  // fy0 = iy0 + 3), stage column -tcol; tile row r adds SW - RP on top of r * RP
+  const uint8_t* const stage_e = stage + 3 * SW - tcol;
   for (int w0 = 0; w0 < total; w0 += cap) {
     if (w0 > 0) __syncthreads();  // the previous round's entries are consumed
     build(w0);
@@ -867,9 +898,9 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_detect(const __grid_co
     const int m_end = min(cap, total - w0);
 #pragma unroll kScoreUnroll
     for (int e = tid; e < m_end; e += kThreads) {
-      const int ent = list[e];
-      const int y = cy_lo + (ent >> 10), xs = ent & 1023;
-      const uint8_t* sp = stage + (y - iy0) * SW + xs;
+      const uint32_t ent = list[e];
+      const uint32_t trow = __umulhi(ent, rp_magic);
+      const uint8_t* sp = stage_e + mad_fma(trow, static_cast<uint32_t>(SW - RP), ent);
       const uint32_t cc = sp[0];
       int sc;
       if (KIND == kSadB) {
@@ -888,7 +919,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_detect(const __grid_co
         for (int i = 0; i < 16; ++i) ring[i] = sp[ring_dy(i) * SW + ring_dx(i)];
         sc = fast_score<N, KIND>(static_cast<int>(cc), ring, P.eps);
       }
-      tile_s[(y - fy0) * RP + xs + tcol] = static_cast<uint16_t>(sc);
+      tile_s[ent] = static_cast<uint16_t>(sc);
     }
   }
   __syncthreads();
@@ -906,12 +937,14 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_detect(const __grid_co
   //        a contiguous range of the list, since tasks are row-major
   unsigned long long n_cand = 0, n_cmp = 0;
   {
-    const int nx_lo = max(x_lo, 3), nx_hi = min(x_hi, w - 3);
-    const unsigned nspan = nx_hi > nx_lo ? static_cast<unsigned>(nx_hi - nx_lo) : 0u;
+    // the tile's own columns [x_lo, x_hi) are tile columns [2n, 2n + span):
+    // the list holds corners of FAST columns only, so one unsigned test on the
+    // tile column drops the halo columns of the neighbouring tiles
+    const unsigned tspan = static_cast<unsigned>(x_hi - x_lo);
     const int e_lo = T1 > T0 ? scan[kWarps + 1] : 0;
     const int e_hi = T1 > T0 ? scan[kWarps + 2] : 0;
     const int rp = RP;
-    const uint32_t kc = static_cast<uint32_t>((1023 + y0) * 1024 + 1023 + x_lo);
+    const int xo = x_lo - 2 * n;  // image x of tile column 0
     // cell map constants; the additive parts and the CTA's first cell row
     // fold into one base slot
     const uint32_t cmx = L.cmx, cmy = L.cmy;
@@ -932,12 +965,11 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_detect(const __grid_co
         constexpr bool LOCAL = decltype(local)::value;
 #pragma unroll kNmsUnroll
         for (int e = w0 + tid; e < m_end; e += kThreads) {
-          const int ent = list[e - off];
-          const int y = cy_lo + (ent >> 10), xs = ent & 1023;
-          const int x = bx0 + xs;
-          // halo column of a neighbouring tile (one unsigned range test)
-          if (static_cast<unsigned>(x - nx_lo) >= nspan) continue;
-          const uint16_t* row = tile_s + (y - fy0) * rp + xs + tcol;
+          const uint32_t ent = list[e - off];
+          const uint32_t trow = __umulhi(ent, rp_magic);
+          const uint32_t xcol = ent - trow * static_cast<uint32_t>(rp);
+          if (xcol - static_cast<uint32_t>(2 * n) >= tspan) continue;  // halo column
+          const uint16_t* row = tile_s + ent;
           const int s = row[0];
           // a corner whose score is 0 (MT, eps 0) is no candidate; a SAD score
           // sums >= N positive terms, so it is > 0 for every corner
@@ -946,6 +978,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_detect(const __grid_co
             bool keep = true;
             ++n_cand;
             uint32_t cmp = 0;
+            const int x = xo + static_cast<int>(xcol), y = fy0 + static_cast<int>(trow);
             for (int rr = 1; rr <= n && keep; ++rr) {
               auto visit = [&](int dx, int dy) {
                 if (!keep) return;
@@ -981,19 +1014,18 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_detect(const __grid_co
               }
             if (!keep) continue;
           }
+          const uint32_t x = static_cast<uint32_t>(xo) + xcol, y = static_cast<uint32_t>(fy0) + trow;
           if (LOCAL) {
             // 32-bit key inside the CTA: score, then smaller y, then smaller x
-            // (the level is fixed per CTA), as s << 20 | (1023 - (y - y0)) << 10
-            // | (1023 - (x - x_lo)), built with IMADs; the cell with one
-            // IMAD.HI per coordinate (no table loads)
-            const uint32_t key = mad_fma(static_cast<uint32_t>(s), P.pow2[20],
-                                         kc - mad_fma(static_cast<uint32_t>(y), P.pow2[10],
-                                                      static_cast<uint32_t>(x)));
-            const uint32_t cx = __umulhi(static_cast<uint32_t>(x), cmx);
-            const uint32_t cy = __umulhi(static_cast<uint32_t>(y), cmy);
+            // (the level is fixed per CTA), as s << 16 | (0xFFFF - entry) --
+            // entries ascend in (y, x) order; the cell with one IMAD.HI per
+            // coordinate (no table loads)
+            const uint32_t key = mad_fma(static_cast<uint32_t>(s), P.pow2[16], ent ^ 0xFFFFu);
+            const uint32_t cx = __umulhi(x, cmx);
+            const uint32_t cy = __umulhi(y, cmy);
             atomicMax(kbase + mad_fma(cy, static_cast<uint32_t>(ccols), cx), key);
           } else {
-            const int X = x << k, Y = y << k;
+            const int X = static_cast<int>(x) << k, Y = static_cast<int>(y) << k;
             atomicMax(P.keys + static_cast<size_t>(f) * P.cells + P.div_ch(Y) * P.cols + P.div_cw(X),
                       pack_key(s, k, X, Y));
           }
@@ -1012,19 +1044,17 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_detect(const __grid_co
           uint32_t key = 0;
           int slot = -1;
           if (e < m_end) {
-            const int ent = list[e - off];
-            const int y = cy_lo + (ent >> 10), xs = ent & 1023;
-            const int x = bx0 + xs;
-            const uint16_t* row = tile_s + (y - fy0) * rp + xs + tcol;
+            const uint32_t ent = list[e - off];
+            const uint32_t trow = __umulhi(ent, rp_magic);
+            const uint32_t xcol = ent - trow * static_cast<uint32_t>(rp);
+            const uint16_t* row = tile_s + ent;
             const int sc = row[0];
             const int e0 = max(max(row[-rp - 1], row[-rp]), max(row[-rp + 1], row[-1]));
             const int l0 = max(max(row[1], row[rp - 1]), max(row[rp], row[rp + 1]));
-            if (x >= nx_lo && x < nx_hi && sc != 0 && e0 < sc && l0 <= sc) {
-              key = mad_fma(static_cast<uint32_t>(sc), P.pow2[20],
-                            kc - mad_fma(static_cast<uint32_t>(y), P.pow2[10], static_cast<uint32_t>(x)));
-              slot = static_cast<int>(mad_fma(__umulhi(static_cast<uint32_t>(y), cmy),
-                                              static_cast<uint32_t>(ccols),
-                                              __umulhi(static_cast<uint32_t>(x), cmx)));
+            if (xcol - static_cast<uint32_t>(2 * n) < tspan && sc != 0 && e0 < sc && l0 <= sc) {
+              const uint32_t x = static_cast<uint32_t>(xo) + xcol, y = static_cast<uint32_t>(fy0) + trow;
+              key = mad_fma(static_cast<uint32_t>(sc), P.pow2[16], ent ^ 0xFFFFu);
+              slot = static_cast<int>(mad_fma(__umulhi(y, cmy), static_cast<uint32_t>(ccols), __umulhi(x, cmx)));
             }
           }
 #if FLKB_KEYS == 1
@@ -1085,10 +1115,12 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_detect(const __grid_co
     // slot row i / ccols: (i + 1/2) / ccols is at least 1/(2 ccols) from an
     // integer, far more than the float error for i < 2^16
     const int rr = __float2int_rz((static_cast<float>(i) + 0.5f) * inv_cc);
-    const int y = y0 + 1023 - static_cast<int>((key >> 10) & 1023u);
-    const int x = x_lo + 1023 - static_cast<int>(key & 1023u);
+    const uint32_t ent = (key & 0xFFFFu) ^ 0xFFFFu;  // the winner's tile index
+    const uint32_t trow = __umulhi(ent, rp_magic);
+    const int y = fy0 + static_cast<int>(trow);
+    const int x = x_lo - 2 * n + static_cast<int>(ent - trow * static_cast<uint32_t>(RP));
     atomicMax(P.keys + static_cast<size_t>(f) * P.cells + (cr0 + rr) * P.cols + cc0 + (i - rr * ccols),
-              pack_key(static_cast<int>(key >> 20), k, x << k, y << k));
+              pack_key(static_cast<int>(key >> 16), k, x << k, y << k));
   }
   phase_end();
 }

@@ -102,11 +102,13 @@ def test_arc_test_exhaustive_on_device(orc, kind, n):
             im[cy[on] + dy, cx[on] + dx] = val[on].astype(np.uint8)
         p = oracle.make_params(epsilon=10, N=n, score_kind=kind)
         det = fl.Detector(fl.Config(epsilon=10, N=n, score_kind=kind))
-        got = det.responses(im, 1)[0][cy, cx]
         expect = np.array([orc.arc_oracle(int(m), n) for m in masks])
-        assert ((got > 0) == expect).all()
         want = orc.fast_level(im, p)[cy, cx]
-        assert (got == want).all()
+        # the staged per-pixel kernel and the fused kernel's bit-sliced masks
+        for fused in (False, True):
+            got = det.responses(im, 1, fused=fused)[0][cy, cx]
+            assert ((got > 0) == expect).all(), f"fused={fused}"
+            assert (got == want).all(), f"fused={fused}"
 
 
 class _DevBuf:

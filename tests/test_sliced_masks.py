@@ -48,6 +48,12 @@ def sliced_less(a, b):
 
 def sliced_arc(m, n):
     w3 = [m[i] & m[(i + 1) % 16] & m[(i + 2) % 16] for i in range(16)]
+    if n == 9:
+        # the kernel's N = 9 form: starts i and i+3 paired along the 16-cycle
+        out = np.zeros_like(m[0])
+        for i in (0, 6, 12, 2, 8, 14, 4, 10):
+            out |= w3[(i + 3) % 16] & w3[(i + 6) % 16] & (w3[i] | w3[(i + 9) % 16])
+        return out
     w9 = [w3[i] & w3[(i + 3) % 16] & w3[(i + 6) % 16] for i in range(16)]
     wn = [w9[i] & w9[(i + n - 9) % 16] for i in range(16)] if n > 9 else w9
     out = np.zeros_like(m[0])
@@ -116,3 +122,23 @@ def test_wrapped_lanes_are_exercised():
     # make sure the biased images contain both at eps = 10
     img = biased_image(np.random.default_rng(1), 40, 83)
     assert (img < 10).mean() > 0.1 and (img > 245).mean() > 0.1
+
+
+@pytest.mark.parametrize("n", range(9, 17))
+def test_sliced_arc_exhaustive(n):
+    """The kernel's bit-sliced segment test (the paired form at N = 9) on all
+    65 536 position masks, 32 masks per lane word, against a plain cyclic run
+    scan (fast.cpp:34-65 builds its LUT the same way)."""
+    masks = np.arange(65536, dtype=np.uint32)
+    want = np.zeros(65536, bool)
+    for s in range(16):
+        run = np.ones(65536, bool)
+        for k in range(n):
+            run &= ((masks >> ((s + k) % 16)) & 1).astype(bool)
+        want |= run
+    lanes = masks.reshape(-1, 32)
+    m = [np.bitwise_or.reduce(((lanes >> i) & 1) << np.arange(32, dtype=np.uint32), axis=1)
+         .astype(np.uint32) for i in range(16)]
+    words = sliced_arc(m, n)
+    got = ((words[:, None] >> np.arange(32, dtype=np.uint32)) & 1).astype(bool).reshape(-1)
+    np.testing.assert_array_equal(got, want)
