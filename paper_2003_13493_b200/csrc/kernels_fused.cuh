@@ -323,39 +323,42 @@ __device__ __forceinline__ void transpose32x8(const uint32_t (&w)[8], uint32_t (
 }
 
 // Bit-sliced segment test: some cyclic run of >= N set positions among the
-// 16 position words (bit lanes = pixels).
+// 16 position words (bit lanes = pixels) iff one of the 8 returned words has
+// the lane set. With w3[i] = m[i] & m[i+1] & m[i+2], a run starting at i is
+// T_i = w3[i] & C_i, C_i = AND m[i+3 .. i+N-1], and the run starting 3 later
+// is C_i & w3[i+N]; so T_i | T_{i+3} = C_i & (w3[i] | w3[i+N]). The 16 starts
+// pair up along the cycle i -> i+3 (gcd(3, 16) = 1): at N = 9 two LOP3 per
+// pair instead of two AND3 and an OR.
 template <int N>
-__device__ __forceinline__ uint32_t sliced_arc(const uint32_t (&m)[16]) {
-  uint32_t w3[16], w9[16];
+__device__ __forceinline__ void sliced_arc_pairs(const uint32_t (&m)[16], uint32_t (&t)[8]) {
+  uint32_t w3[16];
 #pragma unroll
   for (int i = 0; i < 16; ++i) w3[i] = and3(m[i], m[(i + 1) & 15], m[(i + 2) & 15]);
-  if (N == 9) {
-    // runs of 9 start at i: T_i = w3[i] & w3[i+3] & w3[i+6]; two starts 3
-    // apart share two factors, T_i | T_{i+3} = w3[i+3] & w3[i+6] & (w3[i] |
-    // w3[i+9]), and the starts pair up along the 16-cycle i -> i+3 (gcd(3,16)
-    // = 1): two LOP3 per pair instead of two AND3 and an OR
-    uint32_t t[8];
-    constexpr int kPair[8] = {0, 6, 12, 2, 8, 14, 4, 10};
+  constexpr int kPair[8] = {0, 6, 12, 2, 8, 14, 4, 10};
 #pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      const int i = kPair[q];
-      t[q] = and3(w3[(i + 3) & 15], w3[(i + 6) & 15], w3[i] | w3[(i + 9) & 15]);
-    }
-    return or3(or3(t[0], t[1], t[2]), or3(t[3], t[4], t[5]), t[6] | t[7]);
+  for (int q = 0; q < 8; ++q) {
+    const int i = kPair[q];
+    uint32_t c = 0xFFFFFFFFu;
+    int p = 3;
+#pragma unroll
+    for (; p + 3 <= N; p += 3) c &= w3[(i + p) & 15];
+#pragma unroll
+    for (; p < N; ++p) c &= m[(i + p) & 15];
+    t[q] = c & (w3[i] | w3[(i + N) & 15]);
   }
-#pragma unroll
-  for (int i = 0; i < 16; ++i) w9[i] = and3(w3[i], w3[(i + 3) & 15], w3[(i + 6) & 15]);
-  if (N > 9) {
-#pragma unroll
-    for (int i = 0; i < 16; ++i) w3[i] = w9[i] & w9[(i + N - 9) & 15];
-  } else {
-#pragma unroll
-    for (int i = 0; i < 16; ++i) w3[i] = w9[i];
-  }
-  uint32_t a = or3(w3[0], w3[1], w3[2]), b = or3(w3[3], w3[4], w3[5]);
-  uint32_t c = or3(w3[6], w3[7], w3[8]), d = or3(w3[9], w3[10], w3[11]);
-  uint32_t e = or3(w3[12], w3[13], w3[14]);
-  return or3(or3(a, b, c), or3(d, e, w3[15]), 0u);
+}
+
+// Corner lanes of a word: the 16 pair terms of both polarities OR-reduced with
+// seven three-input ORs, the last LOP3 also applying the lane mask.
+template <int N>
+__device__ __forceinline__ uint32_t sliced_corners(const uint32_t (&dk)[16], const uint32_t (&bk)[16],
+                                                   uint32_t valid) {
+  uint32_t d[8], b[8];
+  sliced_arc_pairs<N>(dk, d);
+  sliced_arc_pairs<N>(bk, b);
+  const uint32_t x = or3(or3(d[0], d[1], d[2]), or3(d[3], d[4], d[5]), or3(d[6], d[7], b[0]));
+  const uint32_t y = or3(or3(b[1], b[2], b[3]), or3(b[4], b[5], b[6]), b[7]);
+  return (x | y) & valid;
 }
 
 __device__ __forceinline__ uint32_t vabsdiff4_acc(uint32_t a, uint32_t b, uint32_t acc) {
@@ -736,14 +739,13 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_detect(const __grid_co
         bk[15] = shift_fma(c3.x, -1, P.pow2);
         dk[12] = shift_fma(bk[4], -3, P.pow2);
         bk[12] = shift_fma(dk[4], -3, P.pow2);
-        const uint32_t corner = sliced_arc<N>(dk) | sliced_arc<N>(bk);
         // owned bits [3, 29) that fall inside the FAST columns
         const int xb = bx0 + kOwn * j;
         const int lo_b = max(3, cx_lo - xb), hi_b = min(29, cx_hi - xb);
         const uint32_t valid = hi_b > lo_b ? ((hi_b >= 32 ? 0xFFFFFFFFu : ((1u << hi_b) - 1u)) &
                                               ~((1u << lo_b) - 1u))
                                            : 0u;
-        cm[(y - cy_lo) * nw + j] = corner & valid;
+        cm[(y - cy_lo) * nw + j] = sliced_corners<N>(dk, bk, valid);
       }
       sbase += wave;
       if (sbase >= ring) sbase -= ring;

@@ -47,18 +47,20 @@ def sliced_less(a, b):
 
 
 def sliced_arc(m, n):
+    """The kernel's pair form (kernels_fused.cuh sliced_arc_pairs): starts i
+    and i+3 share C_i = AND m[i+3 .. i+n-1], T_i | T_{i+3} = C_i & (w3[i] | w3[i+n])."""
     w3 = [m[i] & m[(i + 1) % 16] & m[(i + 2) % 16] for i in range(16)]
-    if n == 9:
-        # the kernel's N = 9 form: starts i and i+3 paired along the 16-cycle
-        out = np.zeros_like(m[0])
-        for i in (0, 6, 12, 2, 8, 14, 4, 10):
-            out |= w3[(i + 3) % 16] & w3[(i + 6) % 16] & (w3[i] | w3[(i + 9) % 16])
-        return out
-    w9 = [w3[i] & w3[(i + 3) % 16] & w3[(i + 6) % 16] for i in range(16)]
-    wn = [w9[i] & w9[(i + n - 9) % 16] for i in range(16)] if n > 9 else w9
     out = np.zeros_like(m[0])
-    for v in wn:
-        out |= v
+    for i in (0, 6, 12, 2, 8, 14, 4, 10):
+        c = np.full_like(m[0], 0xFFFFFFFF)
+        p = 3
+        while p + 3 <= n:
+            c &= w3[(i + p) % 16]
+            p += 3
+        while p < n:
+            c &= m[(i + p) % 16]
+            p += 1
+        out |= c & (w3[i] | w3[(i + n) % 16])
     return out
 
 
