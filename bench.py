@@ -35,6 +35,7 @@ other_configs  C1, C2 (single-frame latency), C3, C5 (on every rank) with their
 from __future__ import annotations
 
 import argparse
+import ctypes
 import json
 import os
 import subprocess
@@ -737,18 +738,32 @@ def main():
     # the drop-in-adjacent path: flk_image handles through flkb_detector_run_batch
     # (two-slot pipeline, one flk_features handle per frame), synchronous calls
     hn = min(B, 1024)
-    handle_fps = None
+    handle_fps = mirror_fps = None
     if hn:
         imgs = [fl.Image.from_array(host[i].numpy()) for i in range(hn)]
         det_h = fl.Detector(fl.Config(**CFG), device=local, plan=plan)
         det_h.run_batch(imgs)
+        lib = fl.load_library()
+        arr = (ctypes.c_void_p * hn)(*[i.handle.value for i in imgs])
+        outs = (ctypes.c_void_p * hn)()
         barrier()
-        t0 = time.perf_counter()
-        hsteps = 5
+        # the raw C-ABI call, as a C/C++ consumer of the drop-in makes it: the
+        # call's wall time (H2D from the images' page-locked pixels, kernels,
+        # one flk_features handle per frame); the handles are freed between
+        # calls, outside the timed calls
+        hsteps, th = 5, 0.0
         for _ in range(hsteps):
-            det_h.run_batch(imgs)
-        th = max(max_over_ranks(time.perf_counter() - t0))
+            t0 = time.perf_counter()
+            assert lib.flkb_detector_run_batch(det_h.handle, arr, hn, outs, None) == 0
+            th += time.perf_counter() - t0
+            for i in range(hn):
+                lib.flk_features_destroy(ctypes.c_void_p(outs[i]))
+        th = max(max_over_ranks(th))
         handle_fps = world * hn * hsteps / th
+        # the Python mirror (Detector.run_batch: results copied into numpy arrays)
+        t0 = time.perf_counter()
+        det_h.run_batch(imgs)
+        mirror_fps = world * hn / max(max_over_ranks(time.perf_counter() - t0))
         del imgs
 
     # dominant-kernel time for the roofline: CUDA events around each launch of
@@ -813,7 +828,9 @@ def main():
             "e2e_handles": {"value": handle_fps, "unit": "frames/s",
                             "frames_per_call": hn, "calls": 5,
                             "api": "flkb_detector_run_batch over flk_image handles (page-locked "
-                                   "pixels), one flk_features handle per frame, host wall time"},
+                                   "pixels), one flk_features handle per frame, host wall time "
+                                   "of the raw C-ABI calls",
+                            "python_mirror": mirror_fps},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "kernel": "flkb::fused::k_detect (FAST + score + NMS + cell keys) over "
