@@ -734,6 +734,22 @@ def main():
                                (hfeats.numpy().view(fl.FEATURE_DTYPE).reshape(B, cap) == feats).all()))
     h2d = B * W * H
     d2h = 4 * B + 24 * cap * B
+    # the e2e line's own roof: one pinned H2D copy of the same step's frames
+    # (the PCIe link; CUDA events, best of 3)
+    h2d_gbs = None
+    if B:
+        dcopy = torch.empty_like(host, device="cuda")
+        best = None
+        for _ in range(3):
+            c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            c0.record()
+            dcopy.copy_(host, non_blocking=True)
+            c1.record()
+            torch.cuda.synchronize()
+            ms = c0.elapsed_time(c1)
+            best = ms if best is None else min(best, ms)
+        h2d_gbs = host.numel() / (best / 1e3) / 1e9
+        del dcopy
 
     # the drop-in-adjacent path: flk_image handles through flkb_detector_run_batch
     # (two-slot pipeline, one flk_features handle per frame), synchronous calls
@@ -824,7 +840,14 @@ def main():
                     "api": "flkb_batch_detect_host (pinned host frames in, pinned counts + "
                            "feature lists out; chunked over two streams, H2D and D2H "
                            "overlapped with the kernels)",
-                    "results_equal_device_path": e2e_same},
+                    "results_equal_device_path": e2e_same,
+                    "roofline": {"bound": "pcie_h2d", "unit": "GB/s",
+                                 "achieved": (h2d / 1e9) * e2e_fps / max(G, 1) if G else None,
+                                 "peak": h2d_gbs,
+                                 "frac": ((h2d / 1e9) * e2e_fps / max(G, 1) / h2d_gbs)
+                                 if G and h2d_gbs else None,
+                                 "peak_source": "one pinned host-to-device copy of the step's "
+                                                "frames (torch copy_, CUDA events, best of 3)"}},
             "e2e_handles": {"value": handle_fps, "unit": "frames/s",
                             "frames_per_call": hn, "calls": 5,
                             "api": "flkb_detector_run_batch over flk_image handles (page-locked "

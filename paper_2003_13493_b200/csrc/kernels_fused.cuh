@@ -952,6 +952,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_detect(const __grid_co
     const uint32_t cmx = L.cmx, cmy = L.cmy;
     uint32_t* const kbase = skeys + static_cast<int>(L.ccy - static_cast<uint32_t>(cr0)) * ccols +
                             static_cast<int>(L.ccx) - cc0;
+    const uint32_t kbase_s = static_cast<uint32_t>(__cvta_generic_to_shared(kbase));
     for (int w0 = e_lo; w0 < e_hi; w0 += cap) {
       const bool resident = total <= cap;  // the scoring list is still in place
       const int off = resident ? 0 : w0;
@@ -1025,7 +1026,10 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_detect(const __grid_co
             const uint32_t key = mad_fma(static_cast<uint32_t>(s), P.pow2[16], ent ^ 0xFFFFu);
             const uint32_t cx = __umulhi(x, cmx);
             const uint32_t cy = __umulhi(y, cmy);
-            atomicMax(kbase + mad_fma(cy, static_cast<uint32_t>(ccols), cx), key);
+            // shared byte address of the slot: one IMAD for cy * ccols + cx, one
+            // LEA onto the CTA's (uniform) key base
+            const uint32_t addr = kbase_s + 4u * mad_fma(cy, static_cast<uint32_t>(ccols), cx);
+            asm volatile("red.shared.max.u32 [%0], %1;" ::"r"(addr), "r"(key) : "memory");
           } else {
             const int X = static_cast<int>(x) << k, Y = static_cast<int>(y) << k;
             atomicMax(P.keys + static_cast<size_t>(f) * P.cells + P.div_ch(Y) * P.cols + P.div_cw(X),

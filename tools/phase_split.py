@@ -17,13 +17,13 @@ HELPERS = {"transpose32x8": "2. planes", "sliced_less": "3. masks", "sliced_arc"
            "shl_fma": "2-3 shifts", "shift_fma": "2-3 shifts", "sad_b_packed": "4c. score",
            "vabsdiff4_acc": "4c. score", "FastDiv": "div", "TaskIter": "2-3 task walk"}
 SUB4 = [("4a. count+scan", "const int tasks_f"), ("4b. list build", "auto build = [&](int w0)"),
-        ("4c. score", "const int tcol = bx0"), ]
+        ("4c. score", "const uint32_t rp_magic = RADIUS"), ]
 SUB5 = [("5a. nms", "// --- 5."), ("5b. cell keys", "if (!keep) continue;")]
 
 
 def phase_map():
     lines = open(SRC).read().split("\n")
-    kstart = next(i for i, l in enumerate(lines) if l.startswith("template <int N, int KIND, int RADIUS>"))
+    kstart = next(i for i, l in enumerate(lines) if l.startswith("template <int N, int KIND, int RADIUS, bool STATS>"))
     ph, cur, func = {}, "0. setup", None
     for i, l in enumerate(lines):
         m = re.search(r"// --- (\d\w?)\.\s*(\w+)", l)
