@@ -361,6 +361,22 @@ __device__ __forceinline__ uint32_t sliced_corners(const uint32_t (&dk)[16], con
   return (x | y) & valid;
 }
 
+__device__ __forceinline__ uint32_t bfind(uint32_t m) {  // index of the highest set bit (FLO)
+  uint32_t d;
+  asm("bfind.u32 %0, %1;" : "=r"(d) : "r"(m));
+  return d;
+}
+__device__ __forceinline__ uint32_t bit(uint32_t i) {
+  uint32_t d;
+  asm("bmsk.clamp.b32 %0, %1, 1;" : "=r"(d) : "r"(i));  // 1 << i (BMSK, no constant register)
+  return d;
+}
+__device__ __forceinline__ uint32_t lds_u16(uint32_t shared_addr) {
+  uint16_t v;
+  asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(shared_addr) : "memory");
+  return v;
+}
+
 __device__ __forceinline__ uint32_t vabsdiff4_acc(uint32_t a, uint32_t b, uint32_t acc) {
   uint32_t d;
   asm("vabsdiff4.u32.u32.u32.add %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(acc));
@@ -835,17 +851,17 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_detect(const __grid_co
           // twice to the same slot
           uint16_t* a = list + pos;
           uint16_t* z = list + pos + c - 1;
-          const uint32_t e31 = e0 + 31u;
           while (m) {  // unrolled by two: up to four bits per trip
-            uint32_t lz = __clz(m);
+            // highest set bit hb (FLO), lowest (BREV + FLO.SH); both cleared
+            uint32_t hb = bfind(m);
             a[0] = static_cast<uint16_t>(e0 + (__ffs(m) - 1));
-            z[0] = static_cast<uint16_t>(e31 - lz);
-            m &= (m - 1u) & ~(0x80000000u >> lz);
+            z[0] = static_cast<uint16_t>(e0 + hb);
+            m &= (m - 1u) & ~bit(hb);
             if (!m) break;
-            lz = __clz(m);
+            hb = bfind(m);
             a[1] = static_cast<uint16_t>(e0 + (__ffs(m) - 1));
-            z[-1] = static_cast<uint16_t>(e31 - lz);
-            m &= (m - 1u) & ~(0x80000000u >> lz);
+            z[-1] = static_cast<uint16_t>(e0 + hb);
+            m &= (m - 1u) & ~bit(hb);
             a += 2;
             z -= 2;
           }
@@ -893,14 +909,16 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_detect(const __grid_co
   // stage byte of tile index 0's pixel: stage row 3 (tile row 0 = image row
   // fy0 = iy0 + 3), stage column -tcol; tile row r adds SW - RP on top of r * RP
   const uint8_t* const stage_e = stage + 3 * SW - tcol;
+  const uint32_t list_s = static_cast<uint32_t>(__cvta_generic_to_shared(list));
   for (int w0 = 0; w0 < total; w0 += cap) {
     if (w0 > 0) __syncthreads();  // the previous round's entries are consumed
     build(w0);
     __syncthreads();
     const int m_end = min(cap, total - w0);
+    // shared-address induction: one add per trip for the entry address and the bound
 #pragma unroll kScoreUnroll
-    for (int e = tid; e < m_end; e += kThreads) {
-      const uint32_t ent = list[e];
+    for (uint32_t la = list_s + 2u * tid; la < list_s + 2u * m_end; la += 2u * kThreads) {
+      const uint32_t ent = lds_u16(la);
       const uint32_t trow = __umulhi(ent, rp_magic);
       const uint8_t* sp = stage_e + mad_fma(trow, static_cast<uint32_t>(SW - RP), ent);
       const uint32_t cc = sp[0];
@@ -967,8 +985,9 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_detect(const __grid_co
       auto suppress = [&](auto local) {
         constexpr bool LOCAL = decltype(local)::value;
 #pragma unroll kNmsUnroll
-        for (int e = w0 + tid; e < m_end; e += kThreads) {
-          const uint32_t ent = list[e - off];
+        for (uint32_t la = list_s + 2u * (w0 - off + tid); la < list_s + 2u * (m_end - off);
+             la += 2u * kThreads) {
+          const uint32_t ent = lds_u16(la);
           const uint32_t trow = __umulhi(ent, rp_magic);
           const uint32_t xcol = ent - trow * static_cast<uint32_t>(rp);
           if (xcol - static_cast<uint32_t>(2 * n) >= tspan) continue;  // halo column
