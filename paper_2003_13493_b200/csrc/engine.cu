@@ -335,8 +335,8 @@ fused::Params fused_geometry(const DetectParams& p, const Geometry& g, int R, in
   // the radius-1 instance has compile-time pitches; layouts that fit are padded to them
   if (n == 1 && P.sw <= fused::kSw1 && P.rp <= fused::kRp1) P.sw = fused::kSw1, P.rp = fused::kRp1;
   P.rp_magic = 0xFFFFFFFFu / static_cast<uint32_t>(P.rp) + 1u;  // ceil(2^32 / rp)
-  // 32-bit in-cell keys need cells of at most 1024 px per side
-  // 32-bit in-CTA keys (score << 20 | 10-bit y and x offsets inside the CTA)
+  // 32-bit in-CTA keys (score << 16 | 0xFFFF - the corner's u16 tile index),
+  // one shared slot per cell the CTA touches
   P.key_slots = slots <= 4096 ? slots : 0;
   for (int i = 0; i < 32; ++i) P.pow2[i] = 1u << i;
   for (int b = 0; b < 8; ++b) P.emask[b] = ((p.epsilon >> b) & 1) ? 0xFFFFFFFFu : 0u;
