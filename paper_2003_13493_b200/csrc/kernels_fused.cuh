@@ -383,8 +383,10 @@ __device__ __forceinline__ uint32_t vabsdiff4_acc(uint32_t a, uint32_t b, uint32
   return d;
 }
 
-// SAD-B of one corner from its 16 ring bytes packed 4 per word:
-// sum max(|d|-e,0) = (sum | |d| - e | + sum |d| - 16 e) / 2.
+// Twice the SAD-B of one corner from its 16 ring bytes packed 4 per word:
+// 2 sum max(|d|-e,0) = sum | |d| - e | + sum |d| - 16 e (the score tile holds
+// the doubled scores: the window comparisons are scale-free, and the key's
+// score field takes the doubling as one shift less).
 // acc0 = -16 e (mod 2^32), a constant-bank operand, starts the first sum.
 __device__ __forceinline__ int sad_b_packed(const uint32_t (&r)[4], uint32_t c, uint32_t eps,
                                             uint32_t acc0) {
@@ -396,7 +398,7 @@ __device__ __forceinline__ int sad_b_packed(const uint32_t (&r)[4], uint32_t c, 
     acc1 = vabsdiff4_acc(d, e4, acc1);
     acc2 = vabsdiff4_acc(r[k], c4, acc2);
   }
-  return static_cast<int>((acc1 + acc2) >> 1);
+  return static_cast<int>(acc1 + acc2);
 }
 
 // ---------------------------------------------------------------- kernel
@@ -433,6 +435,8 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_detect(const __grid_co
   // pads the layout to them), so ring and window loads take immediate offsets
   const int SW = RADIUS == 1 ? kSw1 : P.sw;
   const int RP = RADIUS == 1 ? kRp1 : P.rp;
+  // SAD-B scores sit doubled in the score tile (sad_b_packed)
+  constexpr int kTileShift = KIND == kSadB ? 1 : 0;
 
   // --- which level, band and column tile: from the host's table of this
   //     launch's CTAs (level, rows, columns, cell range), else computed
@@ -542,7 +546,13 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_detect(const __grid_co
 #pragma unroll 1
     for (int i = tid; i < slots; i += kThreads) skeys[i] = 0u;
   }
-  __syncthreads();
+  // with the tensor copy, thread 0 armed the mbarrier and warp 0 alone polls
+  // it: a warp-level sync suffices (the CTA barrier after the poll orders the
+  // key clears); the per-row copies and the plain loads need the CTA barrier
+  if (L.tmap_ok)
+    __syncwarp();
+  else
+    __syncthreads();
   if (L.tma || L.tmap_ok) {
     // row copies (one per thread, the barrier is armed) unless the tensor
     // copy is in flight, then one warp waits for the transaction count
@@ -949,7 +959,8 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_detect(const __grid_co
     const int tw = x_hi - x_lo;
     for (int i = tid; i < (y1 - y0) * tw; i += kThreads) {
       const int y = y0 + i / tw, x = x_lo + i % tw;
-      out[static_cast<size_t>(y) * L.dbg_pitch + x] = tile_s[(y - fy0) * RP + (x - x_lo) + 2 * n];
+      out[static_cast<size_t>(y) * L.dbg_pitch + x] =
+          static_cast<uint16_t>(tile_s[(y - fy0) * RP + (x - x_lo) + 2 * n] >> kTileShift);
     }
   }
 
@@ -1042,7 +1053,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_detect(const __grid_co
             // (the level is fixed per CTA), as s << 16 | (0xFFFF - entry) --
             // entries ascend in (y, x) order; the cell with one IMAD.HI per
             // coordinate (no table loads)
-            const uint32_t key = mad_fma(static_cast<uint32_t>(s), P.pow2[16], ent ^ 0xFFFFu);
+            const uint32_t key = mad_fma(static_cast<uint32_t>(s), P.pow2[16 - kTileShift], ent ^ 0xFFFFu);
             const uint32_t cx = __umulhi(x, cmx);
             const uint32_t cy = __umulhi(y, cmy);
             // shared byte address of the slot: one IMAD for cy * ccols + cx, one
@@ -1052,7 +1063,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_detect(const __grid_co
           } else {
             const int X = static_cast<int>(x) << k, Y = static_cast<int>(y) << k;
             atomicMax(P.keys + static_cast<size_t>(f) * P.cells + P.div_ch(Y) * P.cols + P.div_cw(X),
-                      pack_key(s, k, X, Y));
+                      pack_key(s >> kTileShift, k, X, Y));
           }
         }
       };
@@ -1078,7 +1089,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_detect(const __grid_co
             const int l0 = max(max(row[1], row[rp - 1]), max(row[rp], row[rp + 1]));
             if (xcol - static_cast<uint32_t>(2 * n) < tspan && sc != 0 && e0 < sc && l0 <= sc) {
               const uint32_t x = static_cast<uint32_t>(xo) + xcol, y = static_cast<uint32_t>(fy0) + trow;
-              key = mad_fma(static_cast<uint32_t>(sc), P.pow2[16], ent ^ 0xFFFFu);
+              key = mad_fma(static_cast<uint32_t>(sc), P.pow2[16 - kTileShift], ent ^ 0xFFFFu);
               slot = static_cast<int>(mad_fma(__umulhi(y, cmy), static_cast<uint32_t>(ccols), __umulhi(x, cmx)));
             }
           }
