@@ -5,6 +5,7 @@
 # k_detect launches, and the default bench line.
 mkdir -p gpurun_out
 python -m pytest tests -m gpu -x -q > gpurun_out/gputest_final.log 2>&1; tail -2 gpurun_out/gputest_final.log
+python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; tail -1 gpurun_out/smoke.log
 bash tools/sanitize.sh > gpurun_out/sanitize_summary.txt 2>&1; cat gpurun_out/sanitize_summary.txt
 CHUNKS=0 bash tools/traffic_probe.sh > gpurun_out/traffic_summary.txt 2>&1; tail -1 gpurun_out/traffic_summary.txt
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
